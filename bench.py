@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""bench.py — B-scan pixel insertion throughput of the spinevol reconstruction hot path.
+
+Step = one batch reconstruction of the BASELINE cfg2 whole-spine scan (2400 frames of
+512x480 u8 -> 500x267x2000 voxels @ 0.3 mm): PNN insert of every frame (K1), 3x3x3 mean hole
+fill of the union dirty box (K2), depth-band coronal render of the dirty columns (K3, cfg4),
+and for N>1 the NCCL gather of the coronal image.  Volume z-slab-sharded across ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  --impl reference times the reference CPU path (the
+reference's own spinevol::pixel_to_world insert loop, oracle/_ref, else the oracle port) on
+the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "B-scan pixel insertions/sec (G/s)"
+UNIT = "Gpx/s"
+WORKLOAD = ("cfg2 whole-spine linear sweep: 2400 x 512x480 u8 frames -> 500x267x2000 voxels "
+            "@0.3 mm; step = PNN insert + 3x3x3 mean fill + depth-band coronal render (cfg4)")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def _ncpu():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- CPU reference path
+def cpu_reference(wl, frames, poses, nthreads, min_seconds=0.0, max_passes=1):
+    """Time the reference CPU insert (oracle/_ref: spinevol::pixel_to_world per pixel, z-slab
+    threads) on `frames`; falls back to the oracle port where _ref was not built."""
+    from oracle import oracle as O
+    kind = "reference" if O.ref() is not None else "port"
+    times = []
+    t_all = time.perf_counter()
+    g = None
+    acc = None
+    if kind == "reference":  # preallocate + touch the grid outside the timed region
+        acc = (np.ones(wl.dims[::-1], np.uint32), np.ones(wl.dims[::-1], np.uint16))
+    while True:
+        if kind == "reference":
+            t0 = time.perf_counter()
+            O.ref_insert_frames(wl.dims, wl.voxel_mm, wl.origin, frames, poses, wl.calib,
+                                nthreads=nthreads, out=acc)
+            times.append(time.perf_counter() - t0)
+        else:
+            g = g or O.OracleGrid.for_workload(wl)
+            t0 = time.perf_counter()
+            g.insert_frames_mt(frames, poses, wl.calib, nthreads=nthreads)
+            times.append(time.perf_counter() - t0)
+        if len(times) >= max_passes or time.perf_counter() - t_all >= min_seconds:
+            break
+    px = frames.shape[0] * frames.shape[1] * frames.shape[2]
+    return kind, times, px
+
+
+def sample_frames(wl, every):
+    from paper_2412_00058_b200 import synth
+    idx = np.arange(0, wl.nframes, every)
+    frames = np.empty((len(idx), wl.h, wl.w), np.uint8)
+    for i, k in enumerate(idx):
+        frames[i] = synth.synth_frames_np(wl, int(k), 1)[0]
+    return idx, frames
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2412_00058_b200 import synth
+    wl = synth.cfg2()
+    every = args.ref_every
+    idx, frames = sample_frames(wl, every)
+    nth = _ncpu()
+    kind, _, px = cpu_reference(wl, frames[:4], wl.poses[idx[:4]], nth)  # load + page in
+    step_times = []
+    for i in range(args.warmup + args.steps):
+        _, t, px = cpu_reference(wl, frames, wl.poses[idx], nth)
+        if i >= args.warmup:
+            step_times.append(t[0])
+    tot = sum(step_times)
+    value = px * len(step_times) / tot / 1e9
+    sample = ("%d of 2400 cfg2 frames (every %dth, %.1f Mpx) per step; PNN insert only (the "
+              "reference's spinevol::pixel_to_world + SPEC insert loop), %d threads, %s"
+              % (len(idx), every, px / 1e6, nth, _cpu_model()))
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(step_times) * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+           "data": "synthetic (seeded, BASELINE cfg2 generator)",
+           "config": {"workload": WORKLOAD, "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": kind, "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_00058_b200 as pkg
+    from paper_2412_00058_b200 import _abi, synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    wl = synth.cfg2()
+    fill_r, med_r = wl.fill_radius, synth.CFG4_RENDER["median_radius"]
+    ghost = fill_r + med_r
+    nz = wl.dims[2]
+    ob, oe, ab, ae = ((_abi.I32 * world)() for _ in range(4))
+    _abi.check(_abi.lib().svr_plan_slabs(nz, world, ghost, ob, oe, ab, ae))
+    own = (ob[rank], oe[rank])
+    alloc = (ab[rank], ae[rank])
+    desc = wl.grid_desc(*alloc)
+
+    # frame routing: every frame whose conservative box meets this rank's stored slab
+    boxes = [pkg.frame_bounds(wl.grid_desc(), wl.calib, wl.poses[k:k + 1]) for k in range(wl.nframes)]
+    mine = np.array([k for k, b in enumerate(boxes)
+                     if not b.empty() and b.z1 >= alloc[0] and b.z0 < alloc[1]], dtype=np.int64)
+    poses = wl.poses[mine]
+    ub = [min(boxes[k].x0 for k in mine), min(boxes[k].y0 for k in mine),
+          max(min(boxes[k].z0 for k in mine), alloc[0]), max(boxes[k].x1 for k in mine),
+          max(boxes[k].y1 for k in mine), min(max(boxes[k].z1 for k in mine), alloc[1] - 1)]
+    union = _abi.Box(*ub)
+    fill_region = pkg.dilate(union, fill_r)
+    rp = synth.render_params()
+
+    # device-resident frames from the seeded generator
+    k0, k1 = int(mine[0]), int(mine[-1]) + 1
+    span = torch.empty((k1 - k0, wl.h, wl.w), dtype=torch.uint8, device=dev)
+    for a in range(k0, k1, 4096):
+        b = min(k1, a + 4096)
+        _abi.check(_abi.lib().svr_synth_frames(
+            span[a - k0].data_ptr(), wl.w, wl.h, a, b - a, wl.calib,
+            _abi.rigid_ptr(np.ascontiguousarray(wl.poses[a:b])), wl.kind, wl.seed, local, None))
+    frames = span[torch.from_numpy(mine - k0).to(dev)].contiguous() if len(mine) != k1 - k0 else span
+    del span
+    n_my = frames.shape[0]
+    px_frame = wl.w * wl.h
+    total_px = wl.nframes * px_frame  # units of the whole job
+
+    grid = pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, device=local, z_range=alloc)
+    stream = torch.cuda.Stream(device=dev)
+    grid.set_stream(stream.cuda_stream)
+
+    # algorithmic bytes of the insert launch: sum_f (W*H + U_f * 12)
+    U = grid.footprint(frames, poses, wl.calib)
+    alg_bytes = float(n_my * px_frame + 12 * int(U.sum()))
+    grid.clear()
+
+    rows = own[1] - own[0]
+    rows_max = max(oe[r] - ob[r] for r in range(world))
+    gath_src = torch.zeros((2, rows_max, wl.dims[0]), dtype=torch.float32, device=dev)
+    gath_dst = torch.zeros((world, 2, rows_max, wl.dims[0]), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def gather():
+        if world > 1:
+            grid.read_coronal_into(own[0], own[1] - 1, gath_src[0], gath_src[1])
+            dist.all_gather_into_tensor(gath_dst, gath_src)
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.warmup + args.steps)]
+
+    def step(i):
+        e = ev[i]
+        e[0].record(stream)
+        grid.insert_frames(frames, poses, wl.calib)
+        e[1].record(stream)
+        grid.fill_holes(fill_region, fill_r, pkg.FILL_MEAN, count=False)
+        e[2].record(stream)
+        grid.render_coronal(union, rp, fill_r)
+        e[3].record(stream)
+        gather()
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launches0 = grid.stats()["kernel_launches"]
+        clocks = Clocks(local)
+        clocks.start()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.warmup, args.warmup + args.steps):
+            step(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        barrier()
+        launches = grid.stats()["kernel_launches"] - launches0
+        elapsed_ms = allmax(t0.elapsed_time(t1))
+        timed = ev[args.warmup:]
+        ins_ms = allmax(sum(e[0].elapsed_time(e[1]) for e in timed) / args.steps)
+        fill_ms = allmax(sum(e[1].elapsed_time(e[2]) for e in timed) / args.steps)
+        rend_ms = allmax(sum(e[2].elapsed_time(e[3]) for e in timed) / args.steps)
+
+        # ---- e2e through the public API from pinned host frames
+        frames_host = frames.cpu().pin_memory()
+        mean_h = torch.empty((rows, wl.dims[0]), dtype=torch.float32).pin_memory()
+        max_h = torch.empty_like(mean_h).pin_memory()
+        e2e_steps = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            grid.insert_frames(frames_host, poses, wl.calib)
+            grid.fill_holes(fill_region, fill_r, pkg.FILL_MEAN, count=False)
+            grid.render_coronal(union, rp, fill_r)
+            gather()
+            grid.read_coronal_into(own[0], own[1] - 1, mean_h, max_h)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = allmax(time.perf_counter() - w0)
+        h2d = n_my * px_frame + n_my * 224
+        d2h = 2 * rows * wl.dims[0] * 4
+
+        # ---- per-frame incremental latency (insert -> fill(box+1) -> render(box)), rank-local
+        lat_dev, lat_wall = [], []
+        nl = min(args.latency_frames, n_my)
+        mid = max(0, n_my // 2 - nl // 2)
+        le = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
+        for j in range(nl):
+            k = mid + j
+            torch.cuda.synchronize()
+            w = time.perf_counter()
+            le[j][0].record(stream)
+            grid.insert_frames(frames[k], poses[k:k + 1], wl.calib)
+            b = boxes[int(mine[k])]
+            grid.fill_holes(pkg.dilate(b, fill_r), fill_r, pkg.FILL_MEAN, count=False)
+            grid.render_coronal(b, rp, fill_r)
+            le[j][1].record(stream)
+            stream.synchronize()
+            lat_wall.append((time.perf_counter() - w) * 1e3)
+        torch.cuda.synchronize()
+        lat_dev = [a.elapsed_time(b) for a, b in le]
+
+    stats = grid.stats()
+    hbm, peak_src = _peaks()
+    ins_s = ins_ms / 1e3
+    achieved = alg_bytes / ins_s / 1e9
+    value = total_px * args.steps / (elapsed_ms / 1e3) / 1e9
+    e2e_value = total_px * e2e_steps / e2e_s / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        idx, cf = sample_frames(wl, args.cpu_every)
+        nth = _ncpu()
+        kind, times, px = cpu_reference(wl, cf, wl.poses[idx], nth, min_seconds=args.cpu_seconds,
+                                        max_passes=50)
+        cpu = {"value": px * len(times) / sum(times) / 1e9, "unit": UNIT, "cores": nth, "kind": kind,
+               "sample": "%d of 2400 cfg2 frames (every %dth, %.1f Mpx) x %d passes, PNN insert only, "
+                         "%d threads, %s" % (len(idx), args.cpu_every, px / 1e6, len(times), nth,
+                                             _cpu_model())}
+
+    def pct(v, p):
+        s = sorted(v)
+        return s[int(p * (len(s) - 1) + 0.5)] if s else None
+
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "insert_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded Rayleigh speckle + vertebra arcs, BASELINE cfg2 generator)",
+        "config": {"workload": WORKLOAD, "frames": wl.nframes, "frame": [wl.h, wl.w],
+                   "grid": list(wl.dims), "voxel_mm": wl.voxel_mm, "parallelism": "z-slab x%d" % world,
+                   "l2": "no flush: frames (590 MB) and volume (2.1 GB) exceed the 126 MB L2",
+                   "frames_this_rank": int(n_my)},
+        "stages_ms": {"insert": ins_ms, "fill": fill_ms, "render": rend_ms},
+        "insert_only": {"value": total_px / ins_s / 1e9 if world == 1 else None, "unit": UNIT},
+        "roofline": {"bound": "hbm", "kernel": "k_insert (K1)", "achieved": achieved, "peak": hbm,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_model": "sum_f (W*H + 12*U_f), U_f distinct voxels of frame f (mean %.0f)"
+                                    % float(U.mean())},
+        "latency_ms": {"frames": nl, "device_p50": pct(lat_dev, 0.5), "device_p95": pct(lat_dev, 0.95),
+                       "device_max": max(lat_dev) if lat_dev else None, "wall_p50": pct(lat_wall, 0.5),
+                       "wall_p95": pct(lat_wall, 0.95), "wall_max": max(lat_wall) if lat_wall else None,
+                       "what": "one frame: insert + fill(conservative box+1) + render(box), rank-local"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "cpu_baseline": cpu,
+        "exact_fallbacks_per_frame": stats["exact_fallbacks"] / max(stats["frames_inserted"], 1),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    grid.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-every", type=int, default=10, help="reference arm: frame sample stride")
+    ap.add_argument("--cpu-every", type=int, default=8, help="cpu_baseline frame sample stride")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--latency-frames", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

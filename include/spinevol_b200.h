@@ -1,0 +1,208 @@
+/*
+ * spinevol_b200.h — C-ABI drop-in for the incremental volumetric reconstruction
+ * path of the `spinevol` reference (arXiv 2412.00058), implemented with
+ * hand-written sm_100a CUDA kernels.
+ *
+ * The reference API is header-level C++ (namespace spinevol, value types, exceptions).
+ * Its reconstruction module exists only as a specification;
+ * the only executable hot-path arithmetic is the pixel->world chain in
+ * proj/include/spinevol/geometry.hpp.  Each entry point below names the reference
+ * interface it replaces (file:line).  The header-only C++ wrapper
+ * include/spinevol_b200/reconstruct.hpp rebuilds the SPEC signatures on top of it and
+ * rethrows the core.hpp exception types.
+ *
+ * Conventions
+ *   - Every function returns SVR_OK (0) or an error code; the thread-local message is
+ *     svr_last_error().  Codes follow the reference exit-code mapping
+ *     (core.hpp:12-32): 2 invalid input, 3 algorithm failure, 4 I/O,
+ *     plus 5 for CUDA/NCCL failures.  No C++ exception crosses this boundary.
+ *   - Buffers are owned by the caller and may be host (pageable or pinned) or device
+ *     pointers; the library detects which.  Device memory of a volume is owned by
+ *     the handle.  Calls on one handle are serialised onto the handle's stream.
+ *   - Voxel layout: x fastest, then y, then z.  A handle holds the
+ *     global z planes [z_begin, z_end) (a slab; the whole grid when z_begin=0,
+ *     z_end=nz).  All boxes are in GLOBAL voxel indices, inclusive.
+ */
+#ifndef SPINEVOL_B200_H
+#define SPINEVOL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVR_ABI_VERSION 1
+
+/* return codes (core.hpp:12-32 exit-code mapping) */
+#define SVR_OK 0
+#define SVR_E_INVALID 2   /* spinevol::InvalidInput      */
+#define SVR_E_ALGO 3      /* spinevol::AlgorithmFailure  */
+#define SVR_E_IO 4        /* spinevol::IoError           */
+#define SVR_E_CUDA 5      /* device / NCCL failure        */
+
+#define SVR_PROBE_LINEAR 0 /* pixel (col,row) -> (col*sx, row*sy, 0)            geometry.hpp:183 */
+#define SVR_PROBE_FAN 1    /* (line,sample) -> (r sin th, r cos th, 0) */
+
+#define SVR_FILL_MEAN 0   /* BASELINE cfg1/cfg2: mean of non-empty neighbour values, cube radius r */
+#define SVR_FILL_MEDIAN 1 /* lower median of non-empty neighbour values, Chebyshev r */
+
+#define SVR_ACC_PNN 0       /* u32 sum + u16 count per voxel, nearest-voxel insert */
+#define SVR_ACC_TRILINEAR 1 /* f32 weighted sum + f32 weight, 2x2x2 splat (BASELINE cfg5)     */
+
+#define SVR_PROJ_MAX 0
+#define SVR_PROJ_MEAN 1
+
+/* RigidTransform (geometry.hpp:104-140): unit quaternion w,x,y,z + translation mm. */
+typedef struct svr_rigid {
+    double qw, qx, qy, qz;
+    double tx, ty, tz;
+} svr_rigid;
+
+/* ImageCalibration (geometry.hpp:160-176) + probe geometry.
+ * Linear probe: a frame is crop_h rows x crop_w columns, pixel (col,row) ->
+ *   (col*scale_x_mm, row*scale_y_mm, 0)   (geometry.hpp:183).
+ * Convex fan: a frame is crop_h scanlines x crop_w samples (line-major);
+ *   theta_i = deg_to_rad(-angle/2 + angle*(i+0.5)/lines), r_j = r0 + (j+0.5)*(r1-r0)/samples,
+ *   point = (r_j*sin theta_i, r_j*cos theta_i, 0).  Then image_to_transducer, then pose. */
+typedef struct svr_calib {
+    int32_t crop_x, crop_y, crop_w, crop_h;
+    double scale_x_mm, scale_y_mm;
+    svr_rigid image_to_transducer;
+    double latency_ms;
+    int32_t probe; /* SVR_PROBE_* */
+    int32_t reserved0;
+    double fan_angle_deg, fan_r0_mm, fan_r1_mm;
+} svr_calib;
+
+/* VoxelGrid configuration plus the slab this handle stores. */
+typedef struct svr_grid_desc {
+    int32_t nx, ny, nz;  /* global grid dims */
+    int32_t accum;       /* SVR_ACC_* */
+    double voxel_mm;
+    double origin_mm[3]; /* world position of voxel (0,0,0) centre */
+    int32_t z_begin, z_end; /* global planes held by this handle (slab incl. ghosts) */
+} svr_grid_desc;
+
+/* DirtyRegion: inclusive global voxel box, empty iff x0 > x1. */
+typedef struct svr_box {
+    int32_t x0, y0, z0, x1, y1, z1;
+} svr_box;
+
+/* Stats counters. */
+typedef struct svr_stats {
+    uint64_t frames_inserted;
+    uint64_t pixels_inserted;
+    uint64_t pixels_oob;
+    uint64_t pixels_skipped_zero;
+    uint64_t pixels_saturated; /* voxels found above the SPEC caps at readout */
+    uint64_t exact_fallbacks;  /* pixels resolved by the exact fp64 chain (near .5 ties) */
+    uint64_t kernel_launches;  /* kernels this handle launched (all kinds) */
+} svr_stats;
+
+/* Depth-band coronal render (BASELINE cfg4).  Depth axis = grid y, depth(y) = y*voxel_mm.
+ * Column depth d = first argmax over y in [lo,hi] of f(y+1)-f(y); median over a
+ * (2r+1)^2 window of valid column depths; mean and max of f over [d-above, d+below]. */
+typedef struct svr_render_params {
+    double depth_lo_mm, depth_hi_mm;     /* 15, 60 */
+    double band_above_mm, band_below_mm; /* 5, 2   */
+    int32_t median_radius;               /* 2 -> 5x5 */
+    int32_t fill_mode;                   /* SVR_FILL_* used to decode the fill layer */
+} svr_render_params;
+
+typedef struct svr_volume svr_volume;
+
+/* ---------------------------------------------------------------- host-only ---- */
+int svr_abi_version(void);
+const char* svr_last_error(void);
+/* number of visible CUDA devices (0 on a CPU-only host; never fails) */
+int svr_device_count(void);
+
+/* RigidTransform::from_matrix4 (geometry.hpp:245-251 -> Shepperd from_matrix3 :173-190). */
+int svr_pose_from_matrix4(const double m[16], svr_rigid* out);
+/* compose (geometry.hpp:254-256) */
+int svr_compose(const svr_rigid* a, const svr_rigid* b, svr_rigid* out);
+/* interpolate_pose (geometry.hpp:306-321), poses sorted by t_ms. */
+int svr_interpolate_pose(const double* t_ms, const svr_rigid* poses, int n, double t, svr_rigid* out);
+/* pixel_to_world (geometry.hpp:291-297) for the linear probe, fan point for SVR_PROBE_FAN. */
+int svr_pixel_to_world(double col, double row, const svr_calib* calib, const svr_rigid* pose,
+                       double out_mm[3]);
+/* Conservative voxel box a frame can touch (routing to z-slabs); clipped to the global grid. */
+int svr_frame_bounds(const svr_grid_desc* grid, const svr_calib* calib, const svr_rigid* pose,
+                     svr_box* out);
+/* Contiguous z-slab plan for nranks with `ghost` extra planes each side. */
+int svr_plan_slabs(int32_t nz, int32_t nranks, int32_t ghost, int32_t* owned_begin,
+                   int32_t* owned_end, int32_t* alloc_begin, int32_t* alloc_end);
+
+/* ---------------------------------------------------------------- device ------- */
+/* VoxelGrid construction.  device = CUDA ordinal. */
+int svr_create(const svr_grid_desc* desc, int device, svr_volume** out);
+int svr_destroy(svr_volume* vol);
+/* Use an external cudaStream_t (e.g. the caller's) for every later call. NULL = own stream. */
+int svr_set_stream(svr_volume* vol, void* cuda_stream);
+/* zero accumulators, fill layer, render images, stats */
+int svr_clear(svr_volume* vol);
+int svr_sync(svr_volume* vol);
+int svr_get_desc(const svr_volume* vol, svr_grid_desc* out);
+
+/* insert_frame: one frame, returns the tight dirty box (synchronises). */
+int svr_insert_frame(svr_volume* vol, const uint8_t* px, int64_t row_pitch, int32_t w, int32_t h,
+                     const svr_rigid* pose, const svr_calib* calib, int32_t skip_zero,
+                     svr_box* dirty_out);
+/* Batched insert of nframes frames at px + k*frame_stride (host or device memory).
+ * dirty_out (nframes boxes) and union_out may be NULL: then the call is asynchronous. */
+int svr_insert_frames(svr_volume* vol, const uint8_t* px, int64_t row_pitch, int64_t frame_stride,
+                      int32_t w, int32_t h, int32_t nframes, const svr_rigid* poses,
+                      const svr_calib* calib, int32_t skip_zero, svr_box* dirty_out,
+                      svr_box* union_out);
+
+/* fill_holes over exactly `region` (NULL = whole slab).  The fill layer
+ * is a shadow layer: fills never chain.  filled_out may be NULL (asynchronous). */
+int svr_fill_holes(svr_volume* vol, const svr_box* region, int32_t mode, int32_t radius,
+                   int64_t* filled_out);
+
+/* Depth-band coronal render (BASELINE cfg4), incremental: recompute the columns a change
+ * inside `dirty` can affect (dirty (+) fill_radius for depths, (+) median_radius for the
+ * image).  dirty = NULL re-renders every column of the slab. */
+int svr_render_coronal(svr_volume* vol, const svr_box* dirty, int32_t fill_radius,
+                       const svr_render_params* params);
+/* Copy rendered rows z in [z0,z1] (global, inside the slab) as nx-wide row-major images. */
+int svr_read_coronal(svr_volume* vol, int32_t z0, int32_t z1, float* mean_out, float* max_out,
+                     int32_t* depth_out);
+
+/* coronal_projection: u8 max / mean over non-empty voxels along depth_axis
+ * (0=x,1=y,2=z); use_fills also admits filled voxels.  Output is row-major over the two
+ * remaining axes (lower axis fastest). */
+int svr_coronal_projection(svr_volume* vol, int32_t mode, int32_t depth_axis, int32_t use_fills,
+                           uint8_t* out);
+
+/* Accumulator / value readout over an inclusive box (NULL = whole slab), x fastest. */
+int svr_read_accumulators(svr_volume* vol, const svr_box* box, uint32_t* sum_out,
+                          uint16_t* count_out);
+/* VoxelGrid::value = round(sum/count); apply_fills adds rounded fill values. */
+int svr_read_values(svr_volume* vol, const svr_box* box, int32_t apply_fills, uint8_t* out);
+/* raw fill layer: (n << 16) | payload (mean: sum of neighbour values; median: value). */
+int svr_read_fill(svr_volume* vol, const svr_box* box, uint32_t* out);
+/* trilinear volumes: f32 weighted sum and weight */
+int svr_read_trilinear(svr_volume* vol, const svr_box* box, float* wsum_out, float* weight_out);
+
+int svr_get_stats(svr_volume* vol, svr_stats* out);
+
+/* Analysis (not on the hot path): distinct in-slab voxels each frame touches (the U of the
+ * roofline bytes).  Writes nframes counts. */
+int svr_count_footprint(svr_volume* vol, const uint8_t* px, int64_t row_pitch,
+                        int64_t frame_stride, int32_t w, int32_t h, int32_t nframes,
+                        const svr_rigid* poses, const svr_calib* calib, int32_t skip_zero,
+                        int64_t* distinct_out);
+
+/* Synthetic B-scan generator (bench input, BASELINE configs): writes nframes frames of
+ * w x h u8 into device memory `dst` (row pitch w).  kind 0 = linear speckle + bone arcs,
+ * 1 = log-compressed fan speckle + bright band.  Deterministic in (seed, frame). */
+int svr_synth_frames(void* dst, int32_t w, int32_t h, int32_t first_frame, int32_t nframes,
+                     const svr_calib* calib, const svr_rigid* poses, int32_t kind, uint64_t seed,
+                     int device, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPINEVOL_B200_H */

@@ -1,0 +1,601 @@
+/*
+ * svr_oracle.c — CPU restatement of the spinevol reconstruction hot path.
+ * TEST INFRASTRUCTURE ONLY (see svr_oracle.h).  Build: oracle/Makefile
+ * (gcc -O2 -ffp-contract=off: the reference's fp64 operation order, no contraction).
+ */
+#include "svr_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define SUM_CAP 4294967039ull /* sum must stay below 2^32-256 */
+#define COUNT_CAP 65534u      /* count must stay below 2^16-1 */
+
+/* Quat::rotate (geometry.hpp:44-49): t = 2 (u x v); v' = (v + t*w) + u x t. */
+void orc_rotate(const svr_rigid* T, const double v[3], double out[3]) {
+    const double w = T->qw, ux = T->qx, uy = T->qy, uz = T->qz;
+    /* Vec3::cross (core.hpp:52-54) then operator*(2.0) */
+    double cx = uy * v[2] - uz * v[1];
+    double cy = uz * v[0] - ux * v[2];
+    double cz = ux * v[1] - uy * v[0];
+    double tx = cx * 2.0, ty = cy * 2.0, tz = cz * 2.0;
+    /* v + t * w */
+    double ax = v[0] + tx * w, ay = v[1] + ty * w, az = v[2] + tz * w;
+    /* u.cross(t) */
+    double ex = uy * tz - uz * ty;
+    double ey = uz * tx - ux * tz;
+    double ez = ux * ty - uy * tx;
+    out[0] = ax + ex;
+    out[1] = ay + ey;
+    out[2] = az + ez;
+}
+
+/* RigidTransform::apply (geometry.hpp:122): rotation.rotate(p) + translation. */
+void orc_apply(const svr_rigid* T, const double v[3], double out[3]) {
+    double r[3];
+    orc_rotate(T, v, r);
+    out[0] = r[0] + T->tx;
+    out[1] = r[1] + T->ty;
+    out[2] = r[2] + T->tz;
+}
+
+/* pixel_to_world (geometry.hpp:179-185). Returns 0, or 2 for a pixel outside the image. */
+int orc_pixel_to_world(double col, double row, const svr_calib* c, const svr_rigid* pose,
+                       double out[3]) {
+    if (col < 0 || row < 0 || col >= c->crop_w || row >= c->crop_h) return SVR_E_INVALID;
+    double p[3] = {col * c->scale_x_mm, row * c->scale_y_mm, 0.0};
+    double q[3];
+    orc_apply(&c->image_to_transducer, p, q);
+    orc_apply(pose, q, out);
+    return 0;
+}
+
+/* Fan scanline directions; deg_to_rad as core.hpp:109. Pinned in DESIGN.md §3. */
+void orc_fan_table(const svr_calib* c, double* s, double* co) {
+    const int L = c->crop_h;
+    const double A = c->fan_angle_deg;
+    for (int i = 0; i < L; ++i) {
+        double deg = -0.5 * A + A * ((double)i + 0.5) / (double)L;
+        double th = deg * M_PI / 180.0;
+        s[i] = sin(th);
+        co[i] = cos(th);
+    }
+}
+
+static inline void fan_local(int line, int sample, const svr_calib* c, const double* fs,
+                             const double* fc, double p[3]) {
+    double dr = (c->fan_r1_mm - c->fan_r0_mm) / (double)c->crop_w;
+    double r = c->fan_r0_mm + ((double)sample + 0.5) * dr;
+    p[0] = r * fs[line];
+    p[1] = r * fc[line];
+    p[2] = 0.0;
+}
+
+void orc_fan_point(int line, int sample, const svr_calib* c, const double* fs, const double* fc,
+                   const svr_rigid* pose, double out[3]) {
+    double p[3], q[3];
+    fan_local(line, sample, c, fs, fc, p);
+    orc_apply(&c->image_to_transducer, p, q);
+    orc_apply(pose, q, out);
+}
+
+/* Nearest-voxel snap: i = round((p - origin)/voxel), half away from zero.
+ * Returns 1 and the slab-local linear index when inside the stored slab. */
+static inline int snap(const orc_grid* g, const double w[3], int32_t idx[3], int64_t* lin) {
+    double fx = round((w[0] - g->origin[0]) / g->voxel_mm);
+    double fy = round((w[1] - g->origin[1]) / g->voxel_mm);
+    double fz = round((w[2] - g->origin[2]) / g->voxel_mm);
+    if (!(fx >= 0.0 && fx < (double)g->nx)) return 0;
+    if (!(fy >= 0.0 && fy < (double)g->ny)) return 0;
+    if (!(fz >= (double)g->z_begin && fz < (double)g->z_end)) return 0;
+    idx[0] = (int32_t)fx;
+    idx[1] = (int32_t)fy;
+    idx[2] = (int32_t)fz;
+    *lin = ((int64_t)(idx[2] - g->z_begin) * g->ny + idx[1]) * g->nx + idx[0];
+    return 1;
+}
+
+static inline void world_point(int32_t col, int32_t row, const svr_calib* c, const double* fs,
+                               const double* fc, const svr_rigid* pose, double w[3]) {
+    if (c->probe == SVR_PROBE_FAN) {
+        orc_fan_point(row, col, c, fs, fc, pose, w);
+    } else {
+        double p[3] = {(double)col * c->scale_x_mm, (double)row * c->scale_y_mm, 0.0};
+        double q[3];
+        orc_apply(&c->image_to_transducer, p, q);
+        orc_apply(pose, q, w);
+    }
+}
+
+/* insert_frame. Pixels scanned row-major; skip_zero pixels are skipped
+ * before the transform; OOB pixels dropped and counted; caps per SPEC.md:336. */
+int orc_insert_frame(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
+                     const svr_rigid* pose, const svr_calib* c, int32_t skip_zero,
+                     svr_box* dirty) {
+    if (w != c->crop_w || h != c->crop_h) return SVR_E_INVALID;
+    double* fs = NULL;
+    double* fc = NULL;
+    if (c->probe == SVR_PROBE_FAN) {
+        fs = (double*)malloc(sizeof(double) * h);
+        fc = (double*)malloc(sizeof(double) * h);
+        orc_fan_table(c, fs, fc);
+    }
+    svr_box b = {1, 1, 1, 0, 0, 0};
+    int any = 0;
+    for (int32_t r = 0; r < h; ++r) {
+        for (int32_t col = 0; col < w; ++col) {
+            uint8_t v = px[(int64_t)r * pitch + col];
+            if (skip_zero && v == 0) {
+                g->skipped_zero++;
+                continue;
+            }
+            double wp[3];
+            world_point(col, r, c, fs, fc, pose, wp);
+            int32_t idx[3];
+            int64_t lin;
+            if (!snap(g, wp, idx, &lin)) {
+                g->oob++;
+                continue;
+            }
+            if ((uint64_t)g->sum[lin] + v > SUM_CAP || (uint32_t)g->count[lin] + 1u > COUNT_CAP) {
+                g->saturated++;
+                continue;
+            }
+            g->sum[lin] += v;
+            g->count[lin] += 1;
+            g->inserted++;
+            if (!any) {
+                b.x0 = b.x1 = idx[0];
+                b.y0 = b.y1 = idx[1];
+                b.z0 = b.z1 = idx[2];
+                any = 1;
+            } else {
+                if (idx[0] < b.x0) b.x0 = idx[0];
+                if (idx[0] > b.x1) b.x1 = idx[0];
+                if (idx[1] < b.y0) b.y0 = idx[1];
+                if (idx[1] > b.y1) b.y1 = idx[1];
+                if (idx[2] < b.z0) b.z0 = idx[2];
+                if (idx[2] > b.z1) b.z1 = idx[2];
+            }
+        }
+    }
+    g->frames++;
+    free(fs);
+    free(fc);
+    if (dirty) *dirty = b;
+    return 0;
+}
+
+/* ---- multi-threaded variant (CPU baseline): z-slab-partitioned threads ---- */
+typedef struct {
+    orc_grid* g;
+    const uint8_t* px;
+    int64_t pitch, stride;
+    int32_t w, h, nframes, skip_zero, tid, nthreads;
+    const svr_rigid* poses;
+    const svr_calib* c;
+    const double *fs, *fc;
+    uint64_t inserted, skipped;
+} mt_job;
+
+/* z-range (global planes, conservative) a frame can touch: the affine image of the pixel
+ * grid is spanned by its corners (linear) or every scanline's end samples (fan). */
+static void frame_zrange(const orc_grid* g, const svr_calib* c, const double* fs, const double* fc,
+                         const svr_rigid* pose, int32_t w, int32_t h, int32_t* z0, int32_t* z1) {
+    double lo = 1e300, hi = -1e300, wp[3];
+    if (c->probe == SVR_PROBE_FAN) {
+        for (int32_t i = 0; i < h; ++i)
+            for (int e = 0; e < 2; ++e) {
+                world_point(e ? w - 1 : 0, i, c, fs, fc, pose, wp);
+                double u = (wp[2] - g->origin[2]) / g->voxel_mm;
+                if (u < lo) lo = u;
+                if (u > hi) hi = u;
+            }
+    } else {
+        for (int e = 0; e < 4; ++e) {
+            world_point((e & 1) ? w - 1 : 0, (e & 2) ? h - 1 : 0, c, fs, fc, pose, wp);
+            double u = (wp[2] - g->origin[2]) / g->voxel_mm;
+            if (u < lo) lo = u;
+            if (u > hi) hi = u;
+        }
+    }
+    *z0 = (int32_t)floor(lo) - 2;
+    *z1 = (int32_t)ceil(hi) + 2;
+}
+
+/* Thread t owns z planes [zb_t, ze_t) of the slab and inserts every frame whose z-range
+ * meets them, accumulating only its own planes: plain adds, no atomics, deterministic. */
+static void* mt_worker(void* arg) {
+    mt_job* j = (mt_job*)arg;
+    orc_grid* g = j->g;
+    const int32_t nzl = g->z_end - g->z_begin;
+    const int32_t zb = g->z_begin + (int32_t)((int64_t)nzl * j->tid / j->nthreads);
+    const int32_t ze = g->z_begin + (int32_t)((int64_t)nzl * (j->tid + 1) / j->nthreads);
+    for (int32_t k = 0; k < j->nframes; ++k) {
+        int32_t fz0, fz1;
+        frame_zrange(g, j->c, j->fs, j->fc, &j->poses[k], j->w, j->h, &fz0, &fz1);
+        if (fz1 < zb || fz0 >= ze) continue;
+        const uint8_t* f = j->px + (int64_t)k * j->stride;
+        for (int32_t r = 0; r < j->h; ++r) {
+            for (int32_t col = 0; col < j->w; ++col) {
+                uint8_t v = f[(int64_t)r * j->pitch + col];
+                if (j->skip_zero && v == 0) {
+                    if (j->tid == 0) j->skipped++;
+                    continue;
+                }
+                double wp[3];
+                world_point(col, r, j->c, j->fs, j->fc, &j->poses[k], wp);
+                int32_t idx[3];
+                int64_t lin;
+                if (!snap(g, wp, idx, &lin)) continue;
+                if (idx[2] < zb || idx[2] >= ze) continue;
+                g->sum[lin] += v;
+                g->count[lin] += 1;
+                j->inserted++;
+            }
+        }
+    }
+    return NULL;
+}
+
+int orc_insert_frames_mt(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t stride,
+                         int32_t w, int32_t h, int32_t nframes, const svr_rigid* poses,
+                         const svr_calib* c, int32_t skip_zero, int32_t nthreads) {
+    if (w != c->crop_w || h != c->crop_h) return SVR_E_INVALID;
+    if (nthreads < 1) nthreads = 1;
+    double* fs = NULL;
+    double* fc = NULL;
+    if (c->probe == SVR_PROBE_FAN) {
+        fs = (double*)malloc(sizeof(double) * h);
+        fc = (double*)malloc(sizeof(double) * h);
+        orc_fan_table(c, fs, fc);
+    }
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        mt_job jb = {g, px, pitch, stride, w, h, nframes, skip_zero, t, nthreads, poses, c,
+                     fs, fc, 0, 0};
+        jobs[t] = jb;
+        pthread_create(&th[t], NULL, mt_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) {
+        pthread_join(th[t], NULL);
+        g->inserted += jobs[t].inserted;
+        g->skipped_zero += jobs[t].skipped;
+    }
+    /* every non-skipped pixel is either inserted by exactly one owner or out of bounds */
+    {
+        uint64_t nz = 0;
+        for (int32_t k = 0; k < nframes; ++k) {
+            const uint8_t* f = px + (int64_t)k * stride;
+            for (int32_t r = 0; r < h; ++r)
+                for (int32_t col = 0; col < w; ++col)
+                    if (!(skip_zero && f[(int64_t)r * pitch + col] == 0)) nz++;
+        }
+        uint64_t ins = 0;
+        for (int t = 0; t < nthreads; ++t) ins += jobs[t].inserted;
+        g->oob += nz - ins;
+    }
+    g->frames += (uint64_t)nframes;
+    free(jobs);
+    free(th);
+    free(fs);
+    free(fc);
+    return 0;
+}
+
+/* VoxelGrid::value: round(sum/count); integer form, see DESIGN.md §4. */
+static inline uint32_t voxel_value(uint32_t sum, uint32_t count) {
+    return (uint32_t)((2ull * sum + count) / (2ull * count));
+}
+
+static int cmp_u32(const void* a, const void* b) {
+    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* fill_holes: every voxel of `region` is recomputed into the shadow fill
+ * layer.  Non-empty voxels get 0.  Empty voxels with n >= 1 non-empty neighbours (cube of
+ * radius r, self excluded, clipped to the stored slab) get:
+ *   mean   (BASELINE cfg1): (n << 16) | sum of neighbour values
+ *   median:   (n << 16) | lower median of neighbour values (core.hpp:93-99)
+ * Returns the number of filled voxels. */
+int64_t orc_fill_holes(orc_grid* g, const svr_box* region, int32_t mode, int32_t radius) {
+    svr_box b;
+    if (region) {
+        b = *region;
+    } else {
+        svr_box all = {0, 0, g->z_begin, g->nx - 1, g->ny - 1, g->z_end - 1};
+        b = all;
+    }
+    if (b.x0 < 0) b.x0 = 0;
+    if (b.y0 < 0) b.y0 = 0;
+    if (b.z0 < g->z_begin) b.z0 = g->z_begin;
+    if (b.x1 > g->nx - 1) b.x1 = g->nx - 1;
+    if (b.y1 > g->ny - 1) b.y1 = g->ny - 1;
+    if (b.z1 > g->z_end - 1) b.z1 = g->z_end - 1;
+    if (b.x0 > b.x1 || b.y0 > b.y1 || b.z0 > b.z1) return 0;
+    int side = 2 * radius + 1;
+    uint32_t* vals = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)side * side * side);
+    int64_t filled = 0;
+    const int64_t sx = 1, sy = g->nx, sz = (int64_t)g->nx * g->ny;
+    for (int32_t z = b.z0; z <= b.z1; ++z)
+        for (int32_t y = b.y0; y <= b.y1; ++y)
+            for (int32_t x = b.x0; x <= b.x1; ++x) {
+                int64_t lin = (int64_t)(z - g->z_begin) * sz + y * sy + x * sx;
+                if (g->count[lin] != 0) {
+                    g->fill[lin] = 0;
+                    continue;
+                }
+                int n = 0;
+                uint32_t acc = 0;
+                for (int dz = -radius; dz <= radius; ++dz) {
+                    int32_t zz = z + dz;
+                    if (zz < g->z_begin || zz >= g->z_end) continue;
+                    for (int dy = -radius; dy <= radius; ++dy) {
+                        int32_t yy = y + dy;
+                        if (yy < 0 || yy >= g->ny) continue;
+                        for (int dx = -radius; dx <= radius; ++dx) {
+                            int32_t xx = x + dx;
+                            if (xx < 0 || xx >= g->nx) continue;
+                            int64_t l2 = (int64_t)(zz - g->z_begin) * sz + yy * sy + xx;
+                            uint32_t c = g->count[l2];
+                            if (c == 0) continue;
+                            uint32_t v = voxel_value(g->sum[l2], c);
+                            if (mode == SVR_FILL_MEAN) acc += v;
+                            vals[n] = v;
+                            n++;
+                        }
+                    }
+                }
+                if (n == 0) {
+                    g->fill[lin] = 0;
+                    continue;
+                }
+                if (mode == SVR_FILL_MEDIAN) {
+                    qsort(vals, (size_t)n, sizeof(uint32_t), cmp_u32);
+                    acc = vals[(n - 1) / 2];
+                }
+                g->fill[lin] = ((uint32_t)n << 16) | acc;
+                filled++;
+            }
+    free(vals);
+    return filled;
+}
+
+/* f32 value of a voxel for rendering; returns 0 when the voxel is undefined. */
+static inline int voxel_f(const orc_grid* g, int64_t lin, int32_t fill_mode, float* f) {
+    uint32_t c = g->count[lin];
+    if (c) {
+        *f = (float)voxel_value(g->sum[lin], c);
+        return 1;
+    }
+    uint32_t fl = g->fill ? g->fill[lin] : 0;
+    uint32_t n = fl >> 16;
+    if (n == 0) return 0;
+    if (fill_mode == SVR_FILL_MEAN)
+        *f = (float)(fl & 0xFFFFu) / (float)n;
+    else
+        *f = (float)(fl & 0xFFFFu);
+    return 1;
+}
+
+void orc_values(const orc_grid* g, int32_t apply_fills, uint8_t* out) {
+    int64_t n = (int64_t)(g->z_end - g->z_begin) * g->ny * g->nx;
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t c = g->count[i];
+        if (c) {
+            out[i] = (uint8_t)voxel_value(g->sum[i], c);
+        } else if (apply_fills && g->fill && (g->fill[i] >> 16)) {
+            uint32_t nn = g->fill[i] >> 16, s = g->fill[i] & 0xFFFFu;
+            /* mean fills round like value(): (2s+n)/(2n) */
+            out[i] = (uint8_t)((2u * s + nn) / (2u * nn));
+        } else {
+            out[i] = 0;
+        }
+    }
+}
+
+/* Integer render parameters (shared pin with the device host code). */
+void orc_render_ints(const svr_render_params* p, double v, int32_t ny, int32_t* ylo,
+                     int32_t* yhi, int32_t* above, int32_t* below) {
+    int32_t lo = (int32_t)ceil(p->depth_lo_mm / v - 1e-6);
+    int32_t hi = (int32_t)floor(p->depth_hi_mm / v + 1e-6);
+    if (lo < 0) lo = 0;
+    if (hi > ny - 2) hi = ny - 2;
+    *ylo = lo;
+    *yhi = hi;
+    *above = (int32_t)lround(p->band_above_mm / v);
+    *below = (int32_t)lround(p->band_below_mm / v);
+}
+
+static int cmp_i32(const void* a, const void* b) {
+    int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* Depth-band coronal render (BASELINE cfg4), images are (z_end-z_begin) x nx, x fastest.
+ * Incremental: depths recomputed on dirty (+) fill_radius (x,z), median+band on that (+) R. */
+void orc_render(const orc_grid* g, const svr_box* dirty, int32_t fill_radius,
+                const svr_render_params* p, float* mean, float* maxv, int32_t* depth,
+                int32_t* mdepth) {
+    int32_t ylo, yhi, above, below;
+    orc_render_ints(p, g->voxel_mm, g->ny, &ylo, &yhi, &above, &below);
+    const int32_t R = p->median_radius;
+    int32_t dx0 = 0, dx1 = g->nx - 1, dz0 = g->z_begin, dz1 = g->z_end - 1;
+    if (dirty) {
+        if (dirty->x0 > dirty->x1) return;
+        dx0 = dirty->x0 - fill_radius;
+        dx1 = dirty->x1 + fill_radius;
+        dz0 = dirty->z0 - fill_radius;
+        dz1 = dirty->z1 + fill_radius;
+    }
+    int32_t mx0 = dx0 - R, mx1 = dx1 + R, mz0 = dz0 - R, mz1 = dz1 + R;
+#define CLIPX(a) ((a) < 0 ? 0 : ((a) > g->nx - 1 ? g->nx - 1 : (a)))
+#define CLIPZ(a) ((a) < g->z_begin ? g->z_begin : ((a) > g->z_end - 1 ? g->z_end - 1 : (a)))
+    dx0 = CLIPX(dx0); dx1 = CLIPX(dx1); mx0 = CLIPX(mx0); mx1 = CLIPX(mx1);
+    dz0 = CLIPZ(dz0); dz1 = CLIPZ(dz1); mz0 = CLIPZ(mz0); mz1 = CLIPZ(mz1);
+    const int64_t sz = (int64_t)g->nx * g->ny;
+    /* pass 1: column depth = first argmax of the forward gradient */
+    for (int32_t z = dz0; z <= dz1; ++z)
+        for (int32_t x = dx0; x <= dx1; ++x) {
+            int64_t base = (int64_t)(z - g->z_begin) * sz + x;
+            int valid = 0;
+            float prev = 0.0f;
+            if (ylo <= yhi) {
+                float fv;
+                if (voxel_f(g, base + (int64_t)ylo * g->nx, p->fill_mode, &fv)) { prev = fv; valid = 1; }
+            }
+            float best = 0.0f;
+            int32_t arg = -1;
+            for (int32_t y = ylo; y <= yhi; ++y) {
+                float nxt = 0.0f, fv;
+                if (voxel_f(g, base + (int64_t)(y + 1) * g->nx, p->fill_mode, &fv)) { nxt = fv; valid = 1; }
+                float gr = nxt - prev;
+                if (arg < 0 || gr > best) { best = gr; arg = y; }
+                prev = nxt;
+            }
+            depth[(int64_t)(z - g->z_begin) * g->nx + x] = valid ? arg : -1;
+        }
+    /* pass 2: (2R+1)^2 lower median of valid depths, then mean/max over the band */
+    int32_t* win = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * R + 1) * (2 * R + 1));
+    for (int32_t z = mz0; z <= mz1; ++z)
+        for (int32_t x = mx0; x <= mx1; ++x) {
+            int n = 0;
+            for (int32_t zz = z - R; zz <= z + R; ++zz) {
+                if (zz < g->z_begin || zz >= g->z_end) continue;
+                for (int32_t xx = x - R; xx <= x + R; ++xx) {
+                    if (xx < 0 || xx >= g->nx) continue;
+                    int32_t d = depth[(int64_t)(zz - g->z_begin) * g->nx + xx];
+                    if (d >= 0) win[n++] = d;
+                }
+            }
+            int64_t o = (int64_t)(z - g->z_begin) * g->nx + x;
+            int32_t md = -1;
+            if (n) {
+                qsort(win, (size_t)n, sizeof(int32_t), cmp_i32);
+                md = win[(n - 1) / 2];
+            }
+            mdepth[o] = md;
+            float mv = 0.0f, mx = 0.0f;
+            if (md >= 0) {
+                int32_t y0 = md - above, y1 = md + below;
+                if (y0 < 0) y0 = 0;
+                if (y1 > g->ny - 1) y1 = g->ny - 1;
+                int64_t base = (int64_t)(z - g->z_begin) * sz + x;
+                double s = 0.0;
+                int cnt = 0;
+                float m = 0.0f;
+                for (int32_t y = y0; y <= y1; ++y) {
+                    float fv;
+                    if (voxel_f(g, base + (int64_t)y * g->nx, p->fill_mode, &fv)) {
+                        s += (double)fv;
+                        if (cnt == 0 || fv > m) m = fv;
+                        cnt++;
+                    }
+                }
+                if (cnt) {
+                    mv = (float)(s / (double)cnt);
+                    mx = m;
+                }
+            }
+            mean[o] = mv;
+            maxv[o] = mx;
+        }
+    free(win);
+#undef CLIPX
+#undef CLIPZ
+}
+
+/* coronal_projection: max, or mean over non-empty voxels (round like
+ * value()), along depth_axis; empty columns -> 0.  Output over the two remaining axes,
+ * lower-numbered axis fastest. */
+void orc_coronal_projection(const orc_grid* g, int32_t mode, int32_t axis, int32_t use_fills,
+                            uint8_t* out) {
+    int32_t nzl = g->z_end - g->z_begin;
+    int32_t dims[3] = {g->nx, g->ny, nzl};
+    int a0 = axis == 0 ? 1 : 0;
+    int a1 = axis == 2 ? 1 : 2;
+    for (int32_t j = 0; j < dims[a1]; ++j)
+        for (int32_t i = 0; i < dims[a0]; ++i) {
+            uint32_t mx = 0, n = 0;
+            uint64_t s = 0;
+            for (int32_t k = 0; k < dims[axis]; ++k) {
+                int32_t c[3];
+                c[a0] = i;
+                c[a1] = j;
+                c[axis] = k;
+                int64_t lin = ((int64_t)c[2] * g->ny + c[1]) * g->nx + c[0];
+                uint32_t cnt = g->count[lin], v;
+                if (cnt) {
+                    v = voxel_value(g->sum[lin], cnt);
+                } else if (use_fills && g->fill && (g->fill[lin] >> 16)) {
+                    uint32_t nn = g->fill[lin] >> 16, sm = g->fill[lin] & 0xFFFFu;
+                    v = (2u * sm + nn) / (2u * nn);
+                } else {
+                    continue;
+                }
+                if (v > mx) mx = v;
+                s += v;
+                n++;
+            }
+            uint8_t r = 0;
+            if (n) r = mode == SVR_PROJ_MAX ? (uint8_t)mx : (uint8_t)((2 * s + n) / (2ull * n));
+            out[(int64_t)j * dims[a0] + i] = r;
+        }
+}
+
+/* Trilinear splat (BASELINE cfg5): u = (p - origin)/voxel, i0 = floor(u), f = u - i0; the
+ * 8 corners (clipped to the slab) get w = prod(f or 1-f); wsum += w*px, weight += w.
+ * Accumulated in f32 in row-major pixel order (the tolerance test absorbs order). */
+int orc_insert_trilinear(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
+                         const svr_rigid* pose, const svr_calib* c, int32_t skip_zero) {
+    if (w != c->crop_w || h != c->crop_h) return SVR_E_INVALID;
+    double* fs = NULL;
+    double* fc = NULL;
+    if (c->probe == SVR_PROBE_FAN) {
+        fs = (double*)malloc(sizeof(double) * h);
+        fc = (double*)malloc(sizeof(double) * h);
+        orc_fan_table(c, fs, fc);
+    }
+    for (int32_t r = 0; r < h; ++r)
+        for (int32_t col = 0; col < w; ++col) {
+            uint8_t v = px[(int64_t)r * pitch + col];
+            if (skip_zero && v == 0) {
+                g->skipped_zero++;
+                continue;
+            }
+            double wp[3];
+            world_point(col, r, c, fs, fc, pose, wp);
+            double u[3];
+            for (int a = 0; a < 3; ++a) u[a] = (wp[a] - g->origin[a]) / g->voxel_mm;
+            double i0[3], f[3];
+            for (int a = 0; a < 3; ++a) {
+                i0[a] = floor(u[a]);
+                f[a] = u[a] - i0[a];
+            }
+            int hit = 0;
+            for (int k = 0; k < 8; ++k) {
+                double ix = i0[0] + (k & 1), iy = i0[1] + ((k >> 1) & 1), iz = i0[2] + ((k >> 2) & 1);
+                if (!(ix >= 0 && ix < g->nx && iy >= 0 && iy < g->ny && iz >= g->z_begin &&
+                      iz < g->z_end))
+                    continue;
+                double wt = ((k & 1) ? f[0] : 1.0 - f[0]) * (((k >> 1) & 1) ? f[1] : 1.0 - f[1]) *
+                            (((k >> 2) & 1) ? f[2] : 1.0 - f[2]);
+                int64_t lin = (((int64_t)iz - g->z_begin) * g->ny + (int64_t)iy) * g->nx + (int64_t)ix;
+                g->wsum[lin] += (float)(wt * v);
+                g->weight[lin] += (float)wt;
+                hit = 1;
+            }
+            if (hit)
+                g->inserted++;
+            else
+                g->oob++;
+        }
+    g->frames++;
+    free(fs);
+    free(fc);
+    return 0;
+}

@@ -1,0 +1,1189 @@
+// svr_api.cu — host side of the C-ABI (include/spinevol_b200.h): per-frame pose prep,
+// staging of host frames through a pinned double-buffered ring, kernel dispatch, readout.
+// No C++ exception crosses the boundary; errors are codes + thread-local messages.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "svr_kernels.cuh"
+
+using namespace svr;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(SVR_E_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_),   \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+#define CKL()                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(SVR_E_CUDA, "kernel launch failed: %s (%s:%d)",                    \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+    } while (0)
+
+struct svr_volume {
+    svr_grid_desc d{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    cudaStream_t copy_stream = nullptr;
+    long long nvox = 0;
+    ull* acc = nullptr;
+    float2* tri = nullptr;
+    uint32_t* fill = nullptr;
+    int* r_depth = nullptr;
+    int* r_mdepth = nullptr;
+    float* r_mean = nullptr;
+    float* r_max = nullptr;
+    ull* d_stats = nullptr;  // kStCount counters
+    ull* d_counter = nullptr;
+    // per-frame parameter staging
+    FrameParams* h_params = nullptr;
+    FrameParams* d_params = nullptr;
+    int params_cap = 0;
+    cudaEvent_t params_ev = nullptr;
+    int* d_boxes = nullptr;
+    int* h_boxes = nullptr;
+    int boxes_cap = 0;
+    // host-frame staging ring
+    size_t stage_bytes = 0;
+    uint8_t* h_stage[2] = {nullptr, nullptr};
+    uint8_t* d_stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+    cudaEvent_t ev_free[2] = {nullptr, nullptr};
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
+    // fan table
+    double2* d_fan = nullptr;
+    int fan_lines = 0;
+    double fan_angle = 0.0;
+    uint64_t launches = 0;
+    uint64_t frames = 0;
+};
+
+// ---------------------------------------------------------------- host geometry (exact)
+// Rotation of Quat::rotate (geometry.hpp:44-49) as the linear map it computes in real
+// arithmetic, M = I + 2w[u]x + 2(u u^T - |u|^2 I), evaluated in long double.
+static void quat_mat(const svr_rigid& q, long double M[9]) {
+    const long double w = q.qw, x = q.qx, y = q.qy, z = q.qz;
+    const long double n2 = x * x + y * y + z * z;
+    M[0] = 1 + 2 * (x * x - n2);
+    M[1] = 2 * (x * y) - 2 * w * z;
+    M[2] = 2 * (x * z) + 2 * w * y;
+    M[3] = 2 * (y * x) + 2 * w * z;
+    M[4] = 1 + 2 * (y * y - n2);
+    M[5] = 2 * (y * z) - 2 * w * x;
+    M[6] = 2 * (z * x) - 2 * w * y;
+    M[7] = 2 * (z * y) + 2 * w * x;
+    M[8] = 1 + 2 * (z * z - n2);
+}
+
+static void mat_mul(const long double A[9], const long double B[9], long double C[9]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+
+struct Affine {  // u = K + Mv * p, voxel units (no +1/2)
+    long double Mv[9];
+    long double K[3];
+};
+
+static Affine frame_affine(const svr_rigid& pose, const svr_calib& c, const svr_grid_desc& g) {
+    long double Mp[9], Mc[9], Mv[9];
+    quat_mat(pose, Mp);
+    quat_mat(c.image_to_transducer, Mc);
+    mat_mul(Mp, Mc, Mv);
+    Affine a;
+    const long double v = g.voxel_mm;
+    const long double tc[3] = {c.image_to_transducer.tx, c.image_to_transducer.ty,
+                               c.image_to_transducer.tz};
+    const long double tp[3] = {pose.tx, pose.ty, pose.tz};
+    for (int k = 0; k < 3; ++k) {
+        long double r = Mp[3 * k] * tc[0] + Mp[3 * k + 1] * tc[1] + Mp[3 * k + 2] * tc[2];
+        a.K[k] = (r + tp[k] - (long double)g.origin_mm[k]) / v;
+        for (int j = 0; j < 3; ++j) a.Mv[3 * k + j] = Mv[3 * k + j] / v;
+    }
+    return a;
+}
+
+// Fan scanline directions (pin identical to oracle/svr_oracle.c orc_fan_table).
+static void fan_table(const svr_calib& c, std::vector<double>& s, std::vector<double>& co) {
+    const int L = c.crop_h;
+    const double A = c.fan_angle_deg;
+    s.resize(L);
+    co.resize(L);
+    for (int i = 0; i < L; ++i) {
+        double deg = -0.5 * A + A * ((double)i + 0.5) / (double)L;
+        double th = deg * M_PI / 180.0;
+        s[i] = std::sin(th);
+        co[i] = std::cos(th);
+    }
+}
+
+static bool finite_rigid(const svr_rigid& r) {
+    return std::isfinite(r.qw) && std::isfinite(r.qx) && std::isfinite(r.qy) &&
+           std::isfinite(r.qz) && std::isfinite(r.tx) && std::isfinite(r.ty) && std::isfinite(r.tz);
+}
+
+static int check_calib(const svr_calib* c, int32_t w, int32_t h) {
+    if (!c) return fail(SVR_E_INVALID, "calib is NULL");
+    if (c->crop_w <= 0 || c->crop_h <= 0)
+        return fail(SVR_E_INVALID, "calibration crop_rect must be non-empty");
+    if (w != c->crop_w || h != c->crop_h)
+        return fail(SVR_E_INVALID, "frame dims %dx%d do not match calib crop_rect %dx%d", w, h,
+                    c->crop_w, c->crop_h);
+    if (w > 8192 || h > 8192) return fail(SVR_E_INVALID, "frame dims above 8192 are unsupported");
+    if (!finite_rigid(c->image_to_transducer))
+        return fail(SVR_E_INVALID, "calibration transform not finite");
+    if (c->probe == SVR_PROBE_LINEAR) {
+        if (!(c->scale_x_mm > 0.0) || !(c->scale_y_mm > 0.0))
+            return fail(SVR_E_INVALID, "calibration scales must be positive");
+    } else if (c->probe == SVR_PROBE_FAN) {
+        if (!(c->fan_r1_mm > c->fan_r0_mm) || !(c->fan_r0_mm >= 0.0) ||
+            !(c->fan_angle_deg > 0.0 && c->fan_angle_deg < 180.0))
+            return fail(SVR_E_INVALID, "invalid fan geometry");
+    } else {
+        return fail(SVR_E_INVALID, "unknown probe kind %d", c->probe);
+    }
+    return SVR_OK;
+}
+
+static long long to_fixed(long double x, bool* ok) {
+    long double s = x * 4294967296.0L;
+    if (!(std::fabs(s) < 4.0e18L)) {
+        *ok = false;
+        return 0;
+    }
+    return std::llroundl(s);
+}
+
+static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid_desc& g,
+                       FrameParams* fp) {
+    if (!finite_rigid(pose)) return fail(SVR_E_INVALID, "pose not finite");
+    Affine a = frame_affine(pose, c, g);
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) {
+        if (!(std::fabs(a.K[k]) < 1.0e8L)) ok = false;
+        fp->A[k] = to_fixed(a.K[k] + 0.5L, &ok);
+        fp->Dc[k] = to_fixed(a.Mv[3 * k] * (long double)c.scale_x_mm, &ok);
+        fp->Dr[k] = to_fixed(a.Mv[3 * k + 1] * (long double)c.scale_y_mm, &ok);
+        fp->K[k] = (double)a.K[k];
+        for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = (double)a.Mv[3 * k + j];
+    }
+    if (!ok) return fail(SVR_E_INVALID, "pose maps the frame too far from the grid (|u| >= 1e8 voxels)");
+    fp->pose = pose;
+    return SVR_OK;
+}
+
+static DevCalib dev_calib(const svr_calib& c) {
+    DevCalib d{};
+    d.sx = c.scale_x_mm;
+    d.sy = c.scale_y_mm;
+    d.i2t = c.image_to_transducer;
+    d.probe = c.probe;
+    d.lines = c.crop_h;
+    if (c.probe == SVR_PROBE_FAN) {
+        d.r0 = c.fan_r0_mm;
+        d.dr = (c.fan_r1_mm - c.fan_r0_mm) / (double)c.crop_w;
+    }
+    return d;
+}
+
+static GridDev dev_grid(const svr_grid_desc& d) {
+    GridDev g{};
+    g.nx = d.nx;
+    g.ny = d.ny;
+    g.zb = d.z_begin;
+    g.nzl = d.z_end - d.z_begin;
+    g.voxel = d.voxel_mm;
+    for (int k = 0; k < 3; ++k) g.o[k] = d.origin_mm[k];
+    return g;
+}
+
+// Conservative box (global indices) a frame can touch: affine extremes at the image corners
+// (linear) or at every scanline's end samples (fan), widened by one voxel.
+static svr_box frame_box(const svr_grid_desc& g, const svr_calib& c, const svr_rigid& pose) {
+    Affine a = frame_affine(pose, c, g);
+    long double lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = std::numeric_limits<long double>::infinity();
+        hi[k] = -lo[k];
+    }
+    auto add = [&](long double px, long double py) {
+        for (int k = 0; k < 3; ++k) {
+            long double u = a.K[k] + a.Mv[3 * k] * px + a.Mv[3 * k + 1] * py;
+            lo[k] = std::min(lo[k], u);
+            hi[k] = std::max(hi[k], u);
+        }
+    };
+    if (c.probe == SVR_PROBE_FAN) {
+        std::vector<double> s, co;
+        fan_table(c, s, co);
+        const long double dr = ((long double)c.fan_r1_mm - c.fan_r0_mm) / c.crop_w;
+        const long double ra = c.fan_r0_mm + 0.5L * dr, rb = c.fan_r0_mm + (c.crop_w - 0.5L) * dr;
+        for (int i = 0; i < c.crop_h; ++i) {
+            add(ra * s[i], ra * co[i]);
+            add(rb * s[i], rb * co[i]);
+        }
+    } else {
+        const long double X = (long double)(c.crop_w - 1) * c.scale_x_mm;
+        const long double Y = (long double)(c.crop_h - 1) * c.scale_y_mm;
+        add(0, 0);
+        add(X, 0);
+        add(0, Y);
+        add(X, Y);
+    }
+    const int n[3] = {g.nx, g.ny, g.nz};
+    int b0[3], b1[3];
+    bool empty = false;
+    for (int k = 0; k < 3; ++k) {
+        long double l = std::floor(lo[k] + 0.5L) - 1, h = std::floor(hi[k] + 0.5L) + 1;
+        if (!(h >= 0) || !(l <= n[k] - 1)) {
+            empty = true;
+            break;
+        }
+        b0[k] = (int)std::max<long double>(l, 0);
+        b1[k] = (int)std::min<long double>(h, n[k] - 1);
+    }
+    if (empty) return svr_box{1, 1, 1, 0, 0, 0};
+    return svr_box{b0[0], b0[1], b0[2], b1[0], b1[1], b1[2]};
+}
+
+// ---------------------------------------------------------------- host-only ABI
+extern "C" int svr_abi_version(void) { return SVR_ABI_VERSION; }
+
+extern "C" const char* svr_last_error(void) { return g_err.c_str(); }
+
+extern "C" int svr_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static void q_rotate(const svr_rigid& T, const double v[3], double o[3]) {
+    // Quat::rotate, reference op order (host compiled with -ffp-contract=off)
+    const double w = T.qw, ux = T.qx, uy = T.qy, uz = T.qz;
+    double cx = uy * v[2] - uz * v[1], cy = uz * v[0] - ux * v[2], cz = ux * v[1] - uy * v[0];
+    double tx = cx * 2.0, ty = cy * 2.0, tz = cz * 2.0;
+    double ax = v[0] + tx * w, ay = v[1] + ty * w, az = v[2] + tz * w;
+    double ex = uy * tz - uz * ty, ey = uz * tx - ux * tz, ez = ux * ty - uy * tx;
+    o[0] = ax + ex;
+    o[1] = ay + ey;
+    o[2] = az + ez;
+}
+
+static void q_apply(const svr_rigid& T, const double v[3], double o[3]) {
+    double r[3];
+    q_rotate(T, v, r);
+    o[0] = r[0] + T.tx;
+    o[1] = r[1] + T.ty;
+    o[2] = r[2] + T.tz;
+}
+
+static void q_normalize(double q[4]) {
+    double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    for (int i = 0; i < 4; ++i) q[i] = q[i] / n;
+}
+
+extern "C" int svr_pose_from_matrix4(const double m[16], svr_rigid* out) {
+    if (!m || !out) return fail(SVR_E_INVALID, "NULL argument");
+    if (std::abs(m[12]) > 1e-9 || std::abs(m[13]) > 1e-9 || std::abs(m[14]) > 1e-9 ||
+        std::abs(m[15] - 1.0) > 1e-9)
+        return fail(SVR_E_INVALID, "bottom row of homogeneous matrix must be 0 0 0 1");
+    // Shepperd's method (geometry.hpp:173-190) on the row-major rotation block
+    const double r[9] = {m[0], m[1], m[2], m[4], m[5], m[6], m[8], m[9], m[10]};
+    double tr = r[0] + r[4] + r[8];
+    double q[4];
+    if (tr > 0.0) {
+        double s = std::sqrt(tr + 1.0) * 2.0;
+        q[0] = 0.25 * s; q[1] = (r[7] - r[5]) / s; q[2] = (r[2] - r[6]) / s; q[3] = (r[3] - r[1]) / s;
+    } else if (r[0] > r[4] && r[0] > r[8]) {
+        double s = std::sqrt(1.0 + r[0] - r[4] - r[8]) * 2.0;
+        q[0] = (r[7] - r[5]) / s; q[1] = 0.25 * s; q[2] = (r[1] + r[3]) / s; q[3] = (r[2] + r[6]) / s;
+    } else if (r[4] > r[8]) {
+        double s = std::sqrt(1.0 + r[4] - r[0] - r[8]) * 2.0;
+        q[0] = (r[2] - r[6]) / s; q[1] = (r[1] + r[3]) / s; q[2] = 0.25 * s; q[3] = (r[5] + r[7]) / s;
+    } else {
+        double s = std::sqrt(1.0 + r[8] - r[0] - r[4]) * 2.0;
+        q[0] = (r[3] - r[1]) / s; q[1] = (r[2] + r[6]) / s; q[2] = (r[5] + r[7]) / s; q[3] = 0.25 * s;
+    }
+    double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (n == 0.0) return fail(SVR_E_INVALID, "zero quaternion");
+    q_normalize(q);
+    *out = svr_rigid{q[0], q[1], q[2], q[3], m[3], m[7], m[11]};
+    return SVR_OK;
+}
+
+extern "C" int svr_compose(const svr_rigid* a, const svr_rigid* b, svr_rigid* out) {
+    if (!a || !b || !out) return fail(SVR_E_INVALID, "NULL argument");
+    // compose (geometry.hpp:254-256): rotation (a.q * b.q).normalized(), translation a.apply(b.t)
+    double q[4] = {a->qw * b->qw - a->qx * b->qx - a->qy * b->qy - a->qz * b->qz,
+                   a->qw * b->qx + a->qx * b->qw + a->qy * b->qz - a->qz * b->qy,
+                   a->qw * b->qy - a->qx * b->qz + a->qy * b->qw + a->qz * b->qx,
+                   a->qw * b->qz + a->qx * b->qy - a->qy * b->qx + a->qz * b->qw};
+    double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (n == 0.0) return fail(SVR_E_INVALID, "zero quaternion");
+    q_normalize(q);
+    double t[3] = {b->tx, b->ty, b->tz}, o[3];
+    q_apply(*a, t, o);
+    *out = svr_rigid{q[0], q[1], q[2], q[3], o[0], o[1], o[2]};
+    return SVR_OK;
+}
+
+extern "C" int svr_interpolate_pose(const double* t_ms, const svr_rigid* poses, int n, double t,
+                                    svr_rigid* out) {
+    // interpolate_pose (geometry.hpp:306-321) + slerp (:194-212)
+    if (!t_ms || !poses || !out || n <= 0) return fail(SVR_E_INVALID, "empty pose sequence");
+    if (t < t_ms[0] || t > t_ms[n - 1])
+        return fail(SVR_E_INVALID, "pose interpolation time outside sampled range");
+    int i = (int)(std::lower_bound(t_ms, t_ms + n, t) - t_ms);
+    if (t_ms[i] == t) {
+        *out = poses[i];
+        return SVR_OK;
+    }
+    const svr_rigid& hi = poses[i];
+    const svr_rigid& lo = poses[i - 1];
+    double u = (t - t_ms[i - 1]) / (t_ms[i] - t_ms[i - 1]);
+    svr_rigid r;
+    r.tx = lo.tx + (hi.tx - lo.tx) * u;
+    r.ty = lo.ty + (hi.ty - lo.ty) * u;
+    r.tz = lo.tz + (hi.tz - lo.tz) * u;
+    double a[4] = {lo.qw, lo.qx, lo.qy, lo.qz}, b[4] = {hi.qw, hi.qx, hi.qy, hi.qz}, q[4];
+    double d = a[0] * b[0] + a[1] * b[1] + a[2] * b[2] + a[3] * b[3];
+    if (d < 0.0) {
+        for (int k = 0; k < 4; ++k) b[k] = -b[k];
+        d = -d;
+    }
+    if (d > 0.9995) {
+        for (int k = 0; k < 4; ++k) q[k] = a[k] + u * (b[k] - a[k]);
+    } else {
+        double theta = std::acos(std::clamp(d, -1.0, 1.0));
+        double s = std::sin(theta);
+        double wa = std::sin((1.0 - u) * theta) / s;
+        double wb = std::sin(u * theta) / s;
+        for (int k = 0; k < 4; ++k) q[k] = wa * a[k] + wb * b[k];
+    }
+    double nn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (nn == 0.0) return fail(SVR_E_INVALID, "zero quaternion");
+    q_normalize(q);
+    r.qw = q[0]; r.qx = q[1]; r.qy = q[2]; r.qz = q[3];
+    *out = r;
+    return SVR_OK;
+}
+
+extern "C" int svr_pixel_to_world(double col, double row, const svr_calib* c, const svr_rigid* pose,
+                                  double out[3]) {
+    if (!c || !pose || !out) return fail(SVR_E_INVALID, "NULL argument");
+    if (col < 0 || row < 0 || col >= c->crop_w || row >= c->crop_h)
+        return fail(SVR_E_INVALID, "pixel outside B-mode image bounds");
+    double p[3];
+    if (c->probe == SVR_PROBE_FAN) {
+        std::vector<double> s, co;
+        fan_table(*c, s, co);
+        double dr = (c->fan_r1_mm - c->fan_r0_mm) / (double)c->crop_w;
+        double r = c->fan_r0_mm + (std::floor(col) + 0.5) * dr;
+        int li = (int)row;
+        p[0] = r * s[li];
+        p[1] = r * co[li];
+    } else {
+        p[0] = col * c->scale_x_mm;
+        p[1] = row * c->scale_y_mm;
+    }
+    p[2] = 0.0;
+    double q[3];
+    q_apply(c->image_to_transducer, p, q);
+    q_apply(*pose, q, out);
+    return SVR_OK;
+}
+
+static int check_grid(const svr_grid_desc* g) {
+    if (!g) return fail(SVR_E_INVALID, "grid desc is NULL");
+    if (g->nx <= 0 || g->ny <= 0 || g->nz <= 0) return fail(SVR_E_INVALID, "grid dims must be positive");
+    if (!(g->voxel_mm > 0.0) || !std::isfinite(g->voxel_mm))
+        return fail(SVR_E_INVALID, "voxel_mm must be positive");
+    if (g->z_begin < 0 || g->z_end > g->nz || g->z_begin >= g->z_end)
+        return fail(SVR_E_INVALID, "slab [%d,%d) outside [0,%d)", g->z_begin, g->z_end, g->nz);
+    for (int k = 0; k < 3; ++k)
+        if (!std::isfinite(g->origin_mm[k])) return fail(SVR_E_INVALID, "origin not finite");
+    if (g->accum != SVR_ACC_PNN && g->accum != SVR_ACC_TRILINEAR)
+        return fail(SVR_E_INVALID, "unknown accumulator kind %d", g->accum);
+    return SVR_OK;
+}
+
+extern "C" int svr_frame_bounds(const svr_grid_desc* g, const svr_calib* c, const svr_rigid* pose,
+                                svr_box* out) {
+    if (int e = check_grid(g)) return e;
+    if (!c || !pose || !out) return fail(SVR_E_INVALID, "NULL argument");
+    if (int e = check_calib(c, c->crop_w, c->crop_h)) return e;
+    if (!finite_rigid(*pose)) return fail(SVR_E_INVALID, "pose not finite");
+    *out = frame_box(*g, *c, *pose);
+    return SVR_OK;
+}
+
+extern "C" int svr_plan_slabs(int32_t nz, int32_t nranks, int32_t ghost, int32_t* ob, int32_t* oe,
+                              int32_t* ab, int32_t* ae) {
+    if (nz <= 0 || nranks <= 0 || ghost < 0 || nranks > nz)
+        return fail(SVR_E_INVALID, "invalid slab plan nz=%d nranks=%d ghost=%d", nz, nranks, ghost);
+    for (int r = 0; r < nranks; ++r) {
+        int32_t b = (int32_t)((int64_t)nz * r / nranks), e = (int32_t)((int64_t)nz * (r + 1) / nranks);
+        ob[r] = b;
+        oe[r] = e;
+        ab[r] = std::max(0, b - ghost);
+        ae[r] = std::min(nz, e + ghost);
+    }
+    return SVR_OK;
+}
+
+// ---------------------------------------------------------------- device ABI
+#define VOL_CHECK(v)                                                    \
+    do {                                                                \
+        if (!(v)) return fail(SVR_E_INVALID, "volume handle is NULL");   \
+        CK(cudaSetDevice((v)->device));                                 \
+    } while (0)
+
+extern "C" int svr_destroy(svr_volume* v) {
+    if (!v) return SVR_OK;
+    cudaSetDevice(v->device);
+    if (v->stream) cudaStreamSynchronize(v->stream);
+    if (v->copy_stream) cudaStreamSynchronize(v->copy_stream);
+    cudaFree(v->acc);
+    cudaFree(v->tri);
+    cudaFree(v->fill);
+    cudaFree(v->r_depth);
+    cudaFree(v->r_mdepth);
+    cudaFree(v->r_mean);
+    cudaFree(v->r_max);
+    cudaFree(v->d_stats);
+    cudaFree(v->d_counter);
+    cudaFree(v->d_params);
+    cudaFreeHost(v->h_params);
+    cudaFree(v->d_boxes);
+    cudaFreeHost(v->h_boxes);
+    cudaFree(v->d_fan);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(v->d_stage[i]);
+        cudaFreeHost(v->h_stage[i]);
+        if (v->ev_ready[i]) cudaEventDestroy(v->ev_ready[i]);
+        if (v->ev_free[i]) cudaEventDestroy(v->ev_free[i]);
+        if (v->ev_h2d[i]) cudaEventDestroy(v->ev_h2d[i]);
+    }
+    if (v->params_ev) cudaEventDestroy(v->params_ev);
+    if (v->own_stream && v->stream) cudaStreamDestroy(v->stream);
+    if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
+    cudaGetLastError();
+    delete v;
+    return SVR_OK;
+}
+
+extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** out) {
+    if (!out) return fail(SVR_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (int e = check_grid(desc)) return e;
+    int ndev = svr_device_count();
+    if (ndev <= 0) return fail(SVR_E_CUDA, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(SVR_E_INVALID, "device %d out of range", device);
+    svr_volume* v = new svr_volume();
+    v->d = *desc;
+    v->device = device;
+    auto bail = [&](int code) {
+        svr_destroy(v);
+        return code;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(SVR_E_CUDA, "cudaSetDevice failed"));
+    v->nvox = (long long)desc->nx * desc->ny * (desc->z_end - desc->z_begin);
+    const long long ncol = (long long)desc->nx * (desc->z_end - desc->z_begin);
+    cudaError_t e = cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&v->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        if (desc->accum == SVR_ACC_PNN) {
+            e = cudaMalloc(&v->acc, sizeof(ull) * v->nvox);
+            if (e == cudaSuccess) e = cudaMalloc(&v->fill, sizeof(uint32_t) * v->nvox);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_depth, sizeof(int) * ncol);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_mdepth, sizeof(int) * ncol);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_mean, sizeof(float) * ncol);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_max, sizeof(float) * ncol);
+        } else {
+            e = cudaMalloc(&v->tri, sizeof(float2) * v->nvox);
+        }
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&v->d_stats, sizeof(ull) * kStCount);
+    if (e == cudaSuccess) e = cudaMalloc(&v->d_counter, sizeof(ull) * 2);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->params_ev, cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&v->ev_ready[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_free[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_h2d[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(SVR_E_CUDA, "allocation of %lld voxels failed: %s", v->nvox,
+                         cudaGetErrorString(e)));
+    }
+    *out = v;
+    int rc = svr_clear(v);
+    if (rc) {
+        *out = nullptr;
+        return bail(rc);
+    }
+    return SVR_OK;
+}
+
+extern "C" int svr_set_stream(svr_volume* v, void* s) {
+    VOL_CHECK(v);
+    CK(cudaStreamSynchronize(v->stream));
+    if (v->own_stream && v->stream) CK(cudaStreamDestroy(v->stream));
+    if (s) {
+        v->stream = (cudaStream_t)s;
+        v->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking));
+        v->own_stream = true;
+    }
+    return SVR_OK;
+}
+
+extern "C" int svr_clear(svr_volume* v) {
+    VOL_CHECK(v);
+    const long long ncol = (long long)v->d.nx * (v->d.z_end - v->d.z_begin);
+    if (v->acc) CK(cudaMemsetAsync(v->acc, 0, sizeof(ull) * v->nvox, v->stream));
+    if (v->tri) CK(cudaMemsetAsync(v->tri, 0, sizeof(float2) * v->nvox, v->stream));
+    if (v->fill) CK(cudaMemsetAsync(v->fill, 0, sizeof(uint32_t) * v->nvox, v->stream));
+    if (v->r_depth) {
+        CK(cudaMemsetAsync(v->r_depth, 0xFF, sizeof(int) * ncol, v->stream));
+        CK(cudaMemsetAsync(v->r_mdepth, 0xFF, sizeof(int) * ncol, v->stream));
+        CK(cudaMemsetAsync(v->r_mean, 0, sizeof(float) * ncol, v->stream));
+        CK(cudaMemsetAsync(v->r_max, 0, sizeof(float) * ncol, v->stream));
+    }
+    CK(cudaMemsetAsync(v->d_stats, 0, sizeof(ull) * kStCount, v->stream));
+    v->frames = 0;
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+extern "C" int svr_sync(svr_volume* v) {
+    VOL_CHECK(v);
+    CK(cudaStreamSynchronize(v->stream));
+    CK(cudaGetLastError());
+    return SVR_OK;
+}
+
+extern "C" int svr_get_desc(const svr_volume* v, svr_grid_desc* out) {
+    if (!v || !out) return fail(SVR_E_INVALID, "NULL argument");
+    *out = v->d;
+    return SVR_OK;
+}
+
+static int ensure_params(svr_volume* v, int n) {
+    // the previous upload from h_params must have finished before it is rewritten
+    CK(cudaEventSynchronize(v->params_ev));
+    if (n <= v->params_cap) return SVR_OK;
+    int cap = std::max(n, 2 * v->params_cap);
+    CK(cudaStreamSynchronize(v->stream));
+    cudaFree(v->d_params);
+    cudaFreeHost(v->h_params);
+    v->d_params = nullptr;
+    v->h_params = nullptr;
+    v->params_cap = 0;
+    CK(cudaMalloc(&v->d_params, sizeof(FrameParams) * cap));
+    CK(cudaMallocHost(&v->h_params, sizeof(FrameParams) * cap));
+    v->params_cap = cap;
+    return SVR_OK;
+}
+
+static int ensure_boxes(svr_volume* v, int n) {
+    if (n <= v->boxes_cap) return SVR_OK;
+    int cap = std::max(n, 2 * v->boxes_cap);
+    CK(cudaStreamSynchronize(v->stream));
+    cudaFree(v->d_boxes);
+    cudaFreeHost(v->h_boxes);
+    v->d_boxes = nullptr;
+    v->h_boxes = nullptr;
+    v->boxes_cap = 0;
+    CK(cudaMalloc(&v->d_boxes, sizeof(int) * 6 * cap));
+    CK(cudaMallocHost(&v->h_boxes, sizeof(int) * 6 * cap));
+    v->boxes_cap = cap;
+    return SVR_OK;
+}
+
+static int ensure_fan(svr_volume* v, const svr_calib& c) {
+    if (c.probe != SVR_PROBE_FAN) return SVR_OK;
+    if (v->d_fan && v->fan_lines == c.crop_h && v->fan_angle == c.fan_angle_deg) return SVR_OK;
+    std::vector<double> s, co;
+    fan_table(c, s, co);
+    std::vector<double2> t(c.crop_h);
+    for (int i = 0; i < c.crop_h; ++i) t[i] = make_double2(s[i], co[i]);
+    CK(cudaStreamSynchronize(v->stream));
+    cudaFree(v->d_fan);
+    v->d_fan = nullptr;
+    CK(cudaMalloc(&v->d_fan, sizeof(double2) * c.crop_h));
+    CK(cudaMemcpy(v->d_fan, t.data(), sizeof(double2) * c.crop_h, cudaMemcpyHostToDevice));
+    v->fan_lines = c.crop_h;
+    v->fan_angle = c.fan_angle_deg;
+    return SVR_OK;
+}
+
+__global__ void k_box_init(int* b, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        int* p = b + 6 * i;
+        p[0] = p[1] = p[2] = 0x7fffffff;
+        p[3] = p[4] = p[5] = -0x7fffffff - 1;
+    }
+}
+
+template <int kMode, bool kVec, bool kSkip, bool kBox>
+static void launch_insert_t(svr_volume* v, const uint8_t* px, long long pitch, long long fstride,
+                            int w, int h, int n, const FrameParams* fps, const DevCalib& cal,
+                            uint32_t* mark, uint32_t tag, int* boxes, ull* stats) {
+    const int cpr = (w + kChunk - 1) / kChunk;
+    const int chunks = cpr * h;
+    dim3 block(256), grid((chunks + 255) / 256, n);
+    k_insert<kMode, kVec, kSkip, kBox><<<grid, block, 0, v->stream>>>(
+        px, pitch, fstride, w, h, cpr, fps, cal, v->d_fan, dev_grid(v->d), v->acc, v->tri, mark,
+        tag, boxes, stats);
+    v->launches++;
+}
+
+template <int kMode>
+static void launch_insert(svr_volume* v, bool vec, bool skip, bool box, const uint8_t* px,
+                          long long pitch, long long fstride, int w, int h, int n,
+                          const FrameParams* fps, const DevCalib& cal, uint32_t* mark,
+                          uint32_t tag, int* boxes, ull* stats) {
+#define LI(a, b, c) \
+    launch_insert_t<kMode, a, b, c>(v, px, pitch, fstride, w, h, n, fps, cal, mark, tag, boxes, stats)
+    if (vec) {
+        if (skip) { if (box) LI(true, true, true); else LI(true, true, false); }
+        else { if (box) LI(true, false, true); else LI(true, false, false); }
+    } else {
+        if (skip) { if (box) LI(false, true, true); else LI(false, true, false); }
+        else { if (box) LI(false, false, true); else LI(false, false, false); }
+    }
+#undef LI
+}
+
+static bool is_device_ptr(const void* p, bool* pinned) {
+    cudaPointerAttributes a;
+    *pinned = false;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return true;
+    if (a.type == cudaMemoryTypeHost) *pinned = true;
+    return false;
+}
+
+// Launch over frames resident in device memory, chunked to the grid.y limit.
+static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long pitch,
+                         long long fstride, int w, int h, int n, const FrameParams* fps,
+                         const DevCalib& cal, bool skip, bool box, int* boxes, uint32_t* mark,
+                         uint32_t tag, ull* stats) {
+    const bool vec = ((uintptr_t)px % 16 == 0) && (pitch % 16 == 0) && (fstride % 16 == 0) &&
+                     (w % kChunk == 0);
+    for (int k0 = 0; k0 < n; k0 += 65535) {
+        int m = std::min(65535, n - k0);
+        const uint8_t* p = px + (long long)k0 * fstride;
+        if (mode == kModeInsert)
+            launch_insert<kModeInsert>(v, vec, skip, box, p, pitch, fstride, w, h, m, fps + k0, cal,
+                                       mark, tag, boxes ? boxes + 6 * k0 : nullptr, stats);
+        else if (mode == kModeTrilinear)
+            launch_insert<kModeTrilinear>(v, vec, skip, false, p, pitch, fstride, w, h, m, fps + k0,
+                                          cal, mark, tag, nullptr, stats);
+        else
+            launch_insert<kModeFootprint>(v, vec, skip, false, p, pitch, fstride, w, h, m, fps + k0,
+                                          cal, mark, tag, nullptr, stats);
+        CKL();
+    }
+    return SVR_OK;
+}
+
+static int ensure_stage(svr_volume* v, size_t bytes) {
+    if (bytes <= v->stage_bytes) return SVR_OK;
+    CK(cudaStreamSynchronize(v->stream));
+    CK(cudaStreamSynchronize(v->copy_stream));
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(v->d_stage[i]);
+        cudaFreeHost(v->h_stage[i]);
+        v->d_stage[i] = nullptr;
+        v->h_stage[i] = nullptr;
+    }
+    v->stage_bytes = 0;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMalloc(&v->d_stage[i], bytes));
+        CK(cudaMallocHost(&v->h_stage[i], bytes));
+    }
+    v->stage_bytes = bytes;
+    return SVR_OK;
+}
+
+// Common insert driver: params upload, device or staged-host frames, optional boxes.
+static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pitch, int64_t fstride,
+                         int32_t w, int32_t h, int32_t n, const svr_rigid* poses,
+                         const svr_calib* c, int32_t skip_zero, bool want_box, uint32_t* mark,
+                         uint32_t tag, ull* stats) {
+    if (n < 0) return fail(SVR_E_INVALID, "negative frame count");
+    if (n == 0) return SVR_OK;
+    if (!px || !poses) return fail(SVR_E_INVALID, "NULL frames or poses");
+    if (int e = check_calib(c, w, h)) return e;
+    if (pitch < w) return fail(SVR_E_INVALID, "row pitch %lld < width %d", (long long)pitch, w);
+    if (n > 1 && fstride < pitch * (h - 1) + w)
+        return fail(SVR_E_INVALID, "frame stride %lld too small", (long long)fstride);
+    if (int e = ensure_params(v, n)) return e;
+    for (int k = 0; k < n; ++k)
+        if (int e = make_params(poses[k], *c, v->d, &v->h_params[k]))
+            return fail(e, "frame %d: %s", k, g_err.c_str());
+    if (int e = ensure_fan(v, *c)) return e;
+    CK(cudaMemcpyAsync(v->d_params, v->h_params, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
+                       v->stream));
+    CK(cudaEventRecord(v->params_ev, v->stream));
+    const DevCalib cal = dev_calib(*c);
+    int* boxes = nullptr;
+    if (want_box) {
+        if (int e = ensure_boxes(v, n)) return e;
+        boxes = v->d_boxes;
+        k_box_init<<<(n + 255) / 256, 256, 0, v->stream>>>(boxes, n);
+        v->launches++;
+        CKL();
+    }
+    bool pinned = false;
+    if (is_device_ptr(px, &pinned))
+        return insert_device(v, mode, px, pitch, fstride, w, h, n, v->d_params, cal, skip_zero,
+                             want_box, boxes, mark, tag, stats);
+    // host frames: double-buffered pinned staging, H2D on copy_stream overlapped with kernels
+    const long long fb = (long long)w * h;                   // packed frame bytes
+    const long long pfb = (fb + 15) / 16 * 16;               // 16-B aligned frame stride
+    const size_t want = (size_t)std::min<long long>(64ll << 20, pfb * n);
+    if (int e = ensure_stage(v, std::max<size_t>(want, (size_t)pfb))) return e;
+    const int per = (int)std::max<long long>(1, (long long)v->stage_bytes / pfb);
+    const bool contiguous = (pitch == w) && (fstride == fb) && (pfb == fb);
+    int b = 0;
+    for (int k0 = 0; k0 < n; k0 += per, b ^= 1) {
+        const int m = std::min(per, n - k0);
+        const uint8_t* src = px + (long long)k0 * fstride;
+        // wait until the kernel that last read d_stage[b] is done
+        CK(cudaStreamWaitEvent(v->copy_stream, v->ev_free[b], 0));
+        if (pinned) {
+            if (contiguous) {
+                CK(cudaMemcpyAsync(v->d_stage[b], src, (size_t)(pfb * m), cudaMemcpyHostToDevice,
+                                   v->copy_stream));
+            } else {
+                for (int k = 0; k < m; ++k)
+                    CK(cudaMemcpy2DAsync(v->d_stage[b] + k * pfb, w, src + (long long)k * fstride,
+                                         pitch, w, h, cudaMemcpyHostToDevice, v->copy_stream));
+            }
+        } else {
+            // pageable: pack into the pinned staging buffer once the previous copy drained it
+            CK(cudaEventSynchronize(v->ev_h2d[b]));
+            for (int k = 0; k < m; ++k) {
+                uint8_t* dst = v->h_stage[b] + k * pfb;
+                const uint8_t* s = src + (long long)k * fstride;
+                if (pitch == w)
+                    std::memcpy(dst, s, (size_t)fb);
+                else
+                    for (int r = 0; r < h; ++r) std::memcpy(dst + (long long)r * w, s + r * pitch, w);
+            }
+            CK(cudaMemcpyAsync(v->d_stage[b], v->h_stage[b], (size_t)(pfb * m),
+                               cudaMemcpyHostToDevice, v->copy_stream));
+            CK(cudaEventRecord(v->ev_h2d[b], v->copy_stream));
+        }
+        CK(cudaEventRecord(v->ev_ready[b], v->copy_stream));
+        CK(cudaStreamWaitEvent(v->stream, v->ev_ready[b], 0));
+        if (int e = insert_device(v, mode, v->d_stage[b], w, pfb, w, h, m, v->d_params + k0, cal,
+                                  skip_zero, want_box, boxes ? boxes + 6 * k0 : nullptr, mark,
+                                  tag + (uint32_t)k0, stats))
+            return e;
+        CK(cudaEventRecord(v->ev_free[b], v->stream));
+    }
+    return SVR_OK;
+}
+
+static svr_box box_from_dev(const int* b) {
+    if (b[0] > b[3]) return svr_box{1, 1, 1, 0, 0, 0};
+    return svr_box{b[0], b[1], b[2], b[3], b[4], b[5]};
+}
+
+extern "C" int svr_insert_frames(svr_volume* v, const uint8_t* px, int64_t pitch, int64_t fstride,
+                                 int32_t w, int32_t h, int32_t n, const svr_rigid* poses,
+                                 const svr_calib* c, int32_t skip_zero, svr_box* dirty_out,
+                                 svr_box* union_out) {
+    VOL_CHECK(v);
+    const bool want_box = dirty_out || union_out;
+    const int mode = v->d.accum == SVR_ACC_TRILINEAR ? kModeTrilinear : kModeInsert;
+    if (want_box && mode == kModeTrilinear)
+        return fail(SVR_E_INVALID, "dirty boxes are reported for PNN volumes only");
+    if (int e = insert_common(v, mode, px, pitch, fstride, w, h, n, poses, c, skip_zero, want_box,
+                              nullptr, 0, v->d_stats))
+        return e;
+    v->frames += (uint64_t)std::max(n, 0);
+    if (want_box && n > 0) {
+        CK(cudaMemcpyAsync(v->h_boxes, v->d_boxes, sizeof(int) * 6 * n, cudaMemcpyDeviceToHost,
+                           v->stream));
+        CK(cudaStreamSynchronize(v->stream));
+        svr_box u{1, 1, 1, 0, 0, 0};
+        for (int k = 0; k < n; ++k) {
+            svr_box b = box_from_dev(v->h_boxes + 6 * k);
+            if (dirty_out) dirty_out[k] = b;
+            if (b.x0 > b.x1) continue;
+            if (u.x0 > u.x1) {
+                u = b;
+            } else {
+                u.x0 = std::min(u.x0, b.x0); u.y0 = std::min(u.y0, b.y0); u.z0 = std::min(u.z0, b.z0);
+                u.x1 = std::max(u.x1, b.x1); u.y1 = std::max(u.y1, b.y1); u.z1 = std::max(u.z1, b.z1);
+            }
+        }
+        if (union_out) *union_out = u;
+    } else if (union_out) {
+        *union_out = svr_box{1, 1, 1, 0, 0, 0};
+    }
+    return SVR_OK;
+}
+
+extern "C" int svr_insert_frame(svr_volume* v, const uint8_t* px, int64_t pitch, int32_t w,
+                                int32_t h, const svr_rigid* pose, const svr_calib* c,
+                                int32_t skip_zero, svr_box* dirty_out) {
+    svr_box b;
+    int e = svr_insert_frames(v, px, pitch, pitch * h, w, h, 1, pose, c, skip_zero, &b, nullptr);
+    if (e) return e;
+    if (dirty_out) *dirty_out = b;
+    return SVR_OK;
+}
+
+static bool clip_box(const svr_volume* v, const svr_box* in, Box* out) {
+    svr_box b = in ? *in : svr_box{0, 0, v->d.z_begin, v->d.nx - 1, v->d.ny - 1, v->d.z_end - 1};
+    b.x0 = std::max(b.x0, 0);
+    b.y0 = std::max(b.y0, 0);
+    b.z0 = std::max(b.z0, v->d.z_begin);
+    b.x1 = std::min(b.x1, v->d.nx - 1);
+    b.y1 = std::min(b.y1, v->d.ny - 1);
+    b.z1 = std::min(b.z1, v->d.z_end - 1);
+    *out = Box{b.x0, b.y0, b.z0, b.x1, b.y1, b.z1};
+    return b.x0 <= b.x1 && b.y0 <= b.y1 && b.z0 <= b.z1;
+}
+
+extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode, int32_t radius,
+                              int64_t* filled_out) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "fill_holes needs a PNN volume");
+    if (mode != SVR_FILL_MEAN && mode != SVR_FILL_MEDIAN) return fail(SVR_E_INVALID, "unknown fill mode");
+    if (radius < 1 || radius > 8) return fail(SVR_E_INVALID, "fill radius must be in [1,8]");
+    if (mode == SVR_FILL_MEAN && (2 * radius + 1) * (2 * radius + 1) * (2 * radius + 1) * 255 > 65535)
+        return fail(SVR_E_INVALID, "mean fill radius too large for the 16-bit fill payload");
+    Box b;
+    const bool any = clip_box(v, region, &b);
+    if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
+    if (any) {
+        const GridDev g = dev_grid(v->d);
+        const int bx = b.x1 - b.x0 + 1, by = b.y1 - b.y0 + 1, bz = b.z1 - b.z0 + 1;
+        if (radius == 1) {
+            dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 15) / 16);
+            if (mode == SVR_FILL_MEAN)
+                k_fill<1, SVR_FILL_MEAN, 32, 8, 16><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+            else
+                k_fill<1, SVR_FILL_MEDIAN, 32, 8, 16><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+        } else if (radius == 2) {
+            dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 7) / 8);
+            if (mode == SVR_FILL_MEAN)
+                k_fill<2, SVR_FILL_MEAN, 32, 8, 8><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+            else
+                k_fill<2, SVR_FILL_MEDIAN, 32, 8, 8><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+        } else {
+            long long nv = (long long)bx * by * bz;
+            k_fill_generic<<<(unsigned)((nv + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, g, b, radius, mode, v->d_counter);
+        }
+        v->launches++;
+        CKL();
+    }
+    if (filled_out) {
+        ull c = 0;
+        CK(cudaMemcpyAsync(&c, v->d_counter, sizeof(ull), cudaMemcpyDeviceToHost, v->stream));
+        CK(cudaStreamSynchronize(v->stream));
+        *filled_out = (int64_t)c;
+    }
+    return SVR_OK;
+}
+
+// Integer render parameters — identical formula to oracle orc_render_ints.
+static void render_ints(const svr_render_params* p, double vx, int ny, int* ylo, int* yhi,
+                        int* above, int* below) {
+    int lo = (int)std::ceil(p->depth_lo_mm / vx - 1e-6);
+    int hi = (int)std::floor(p->depth_hi_mm / vx + 1e-6);
+    if (lo < 0) lo = 0;
+    if (hi > ny - 2) hi = ny - 2;
+    *ylo = lo;
+    *yhi = hi;
+    *above = (int)std::lround(p->band_above_mm / vx);
+    *below = (int)std::lround(p->band_below_mm / vx);
+}
+
+extern "C" int svr_render_coronal(svr_volume* v, const svr_box* dirty, int32_t fill_radius,
+                                  const svr_render_params* p) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "render needs a PNN volume");
+    if (!p) return fail(SVR_E_INVALID, "render params NULL");
+    if (p->median_radius < 0 || p->median_radius > 2)
+        return fail(SVR_E_INVALID, "median_radius must be 0, 1 or 2");
+    if (fill_radius < 0) return fail(SVR_E_INVALID, "negative fill radius");
+    int ylo, yhi, above, below;
+    render_ints(p, v->d.voxel_mm, v->d.ny, &ylo, &yhi, &above, &below);
+    const int R = p->median_radius;
+    const int zb = v->d.z_begin, ze = v->d.z_end - 1, nxm = v->d.nx - 1;
+    int dx0 = 0, dx1 = nxm, dz0 = zb, dz1 = ze;
+    if (dirty) {
+        if (dirty->x0 > dirty->x1) return SVR_OK;
+        dx0 = dirty->x0 - fill_radius;
+        dx1 = dirty->x1 + fill_radius;
+        dz0 = dirty->z0 - fill_radius;
+        dz1 = dirty->z1 + fill_radius;
+    }
+    int mx0 = dx0 - R, mx1 = dx1 + R, mz0 = dz0 - R, mz1 = dz1 + R;
+    auto cx = [&](int a) { return std::min(std::max(a, 0), nxm); };
+    auto cz = [&](int a) { return std::min(std::max(a, zb), ze); };
+    dx0 = cx(dx0); dx1 = cx(dx1); mx0 = cx(mx0); mx1 = cx(mx1);
+    dz0 = cz(dz0); dz1 = cz(dz1); mz0 = cz(mz0); mz1 = cz(mz1);
+    if (dirty && (dirty->x1 < 0 || dirty->x0 > nxm || dirty->z1 + fill_radius + R < zb ||
+                  dirty->z0 - fill_radius - R > ze))
+        return SVR_OK;
+    const GridDev g = dev_grid(v->d);
+    for (int z0 = dz0; z0 <= dz1; z0 += 65535) {
+        int nzs = std::min(65535, dz1 - z0 + 1);
+        dim3 grd((dx1 - dx0 + 1 + 127) / 128, nzs);
+        k_depth<<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dx0, dx1, z0, ylo, yhi, p->fill_mode,
+                                            v->r_depth);
+        v->launches++;
+        CKL();
+    }
+    for (int z0 = mz0; z0 <= mz1; z0 += 65535) {
+        int nzs = std::min(65535, mz1 - z0 + 1);
+        dim3 grd((mx1 - mx0 + 1 + 127) / 128, nzs);
+        k_band<<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, mx0, mx1, z0, R, above, below,
+                                           p->fill_mode, v->r_depth, v->r_mdepth, v->r_mean, v->r_max);
+        v->launches++;
+        CKL();
+    }
+    return SVR_OK;
+}
+
+extern "C" int svr_read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv,
+                                int32_t* depth) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "render needs a PNN volume");
+    if (z0 < v->d.z_begin || z1 >= v->d.z_end || z0 > z1)
+        return fail(SVR_E_INVALID, "rows [%d,%d] outside slab [%d,%d)", z0, z1, v->d.z_begin, v->d.z_end);
+    const size_t off = (size_t)(z0 - v->d.z_begin) * v->d.nx, cnt = (size_t)(z1 - z0 + 1) * v->d.nx;
+    if (mean) CK(cudaMemcpyAsync(mean, v->r_mean + off, cnt * sizeof(float), cudaMemcpyDefault, v->stream));
+    if (maxv) CK(cudaMemcpyAsync(maxv, v->r_max + off, cnt * sizeof(float), cudaMemcpyDefault, v->stream));
+    if (depth) CK(cudaMemcpyAsync(depth, v->r_mdepth + off, cnt * sizeof(int), cudaMemcpyDefault, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+extern "C" int svr_coronal_projection(svr_volume* v, int32_t mode, int32_t axis, int32_t use_fills,
+                                      uint8_t* out) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "projection needs a PNN volume");
+    if (axis < 0 || axis > 2) return fail(SVR_E_INVALID, "depth_axis must be 0, 1 or 2");
+    if (mode != SVR_PROJ_MAX && mode != SVR_PROJ_MEAN) return fail(SVR_E_INVALID, "unknown projection mode");
+    if (!out) return fail(SVR_E_INVALID, "out is NULL");
+    const int dims[3] = {v->d.nx, v->d.ny, v->d.z_end - v->d.z_begin};
+    const int a0 = axis == 0 ? 1 : 0, a1 = axis == 2 ? 1 : 2;
+    const long long n = (long long)dims[a0] * dims[a1];
+    uint8_t* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, n, v->stream));
+    k_project<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, dev_grid(v->d), axis,
+                                                                 mode, use_fills, tmp);
+    v->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(out, tmp, n, cudaMemcpyDefault, v->stream));
+    CK(cudaFreeAsync(tmp, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+static int read_box_common(svr_volume* v, const svr_box* box, Box* b, long long* n) {
+    if (box && (box->x0 < 0 || box->y0 < 0 || box->z0 < v->d.z_begin || box->x1 >= v->d.nx ||
+                box->y1 >= v->d.ny || box->z1 >= v->d.z_end || box->x0 > box->x1 ||
+                box->y0 > box->y1 || box->z0 > box->z1))
+        return fail(SVR_E_INVALID, "box outside the stored slab or empty");
+    clip_box(v, box, b);
+    *n = (long long)(b->x1 - b->x0 + 1) * (b->y1 - b->y0 + 1) * (b->z1 - b->z0 + 1);
+    return SVR_OK;
+}
+
+extern "C" int svr_read_accumulators(svr_volume* v, const svr_box* box, uint32_t* sum, uint16_t* cnt) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "not a PNN volume");
+    Box b;
+    long long n;
+    if (int e = read_box_common(v, box, &b, &n)) return e;
+    uint32_t* ts = nullptr;
+    uint16_t* tc = nullptr;
+    if (sum) CK(cudaMallocAsync(&ts, n * 4, v->stream));
+    if (cnt) CK(cudaMallocAsync(&tc, n * 2, v->stream));
+    CK(cudaMemsetAsync(v->d_counter + 1, 0, sizeof(ull), v->stream));
+    k_read_acc<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, dev_grid(v->d), b, ts, tc,
+                                                                  v->d_counter + 1);
+    v->launches++;
+    CKL();
+    if (sum) CK(cudaMemcpyAsync(sum, ts, n * 4, cudaMemcpyDefault, v->stream));
+    if (cnt) CK(cudaMemcpyAsync(cnt, tc, n * 2, cudaMemcpyDefault, v->stream));
+    ull sat = 0;
+    CK(cudaMemcpyAsync(&sat, v->d_counter + 1, sizeof(ull), cudaMemcpyDeviceToHost, v->stream));
+    if (ts) CK(cudaFreeAsync(ts, v->stream));
+    if (tc) CK(cudaFreeAsync(tc, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    if (sat) {
+        // record in stats: voxels above the caps at readout
+        ull h[kStCount];
+        CK(cudaMemcpy(h, v->d_stats, sizeof h, cudaMemcpyDeviceToHost));
+        h[kStSaturated] = sat;
+        CK(cudaMemcpy(v->d_stats, h, sizeof h, cudaMemcpyHostToDevice));
+    }
+    return SVR_OK;
+}
+
+extern "C" int svr_read_values(svr_volume* v, const svr_box* box, int32_t apply_fills, uint8_t* out) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "not a PNN volume");
+    if (!out) return fail(SVR_E_INVALID, "out is NULL");
+    Box b;
+    long long n;
+    if (int e = read_box_common(v, box, &b, &n)) return e;
+    uint8_t* t = nullptr;
+    CK(cudaMallocAsync(&t, n, v->stream));
+    k_read_values<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, dev_grid(v->d), b,
+                                                                     apply_fills, t);
+    v->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(out, t, n, cudaMemcpyDefault, v->stream));
+    CK(cudaFreeAsync(t, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+extern "C" int svr_read_fill(svr_volume* v, const svr_box* box, uint32_t* out) {
+    VOL_CHECK(v);
+    if (!v->fill) return fail(SVR_E_INVALID, "not a PNN volume");
+    if (!out) return fail(SVR_E_INVALID, "out is NULL");
+    Box b;
+    long long n;
+    if (int e = read_box_common(v, box, &b, &n)) return e;
+    uint32_t* t = nullptr;
+    CK(cudaMallocAsync(&t, n * 4, v->stream));
+    k_read_box<uint32_t><<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->fill, dev_grid(v->d), b, t);
+    v->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(out, t, n * 4, cudaMemcpyDefault, v->stream));
+    CK(cudaFreeAsync(t, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+extern "C" int svr_read_trilinear(svr_volume* v, const svr_box* box, float* ws, float* wt) {
+    VOL_CHECK(v);
+    if (!v->tri) return fail(SVR_E_INVALID, "not a trilinear volume");
+    Box b;
+    long long n;
+    if (int e = read_box_common(v, box, &b, &n)) return e;
+    float *a = nullptr, *c = nullptr;
+    if (ws) CK(cudaMallocAsync(&a, n * 4, v->stream));
+    if (wt) CK(cudaMallocAsync(&c, n * 4, v->stream));
+    k_read_tri<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->tri, dev_grid(v->d), b, a, c);
+    v->launches++;
+    CKL();
+    if (ws) CK(cudaMemcpyAsync(ws, a, n * 4, cudaMemcpyDefault, v->stream));
+    if (wt) CK(cudaMemcpyAsync(wt, c, n * 4, cudaMemcpyDefault, v->stream));
+    if (a) CK(cudaFreeAsync(a, v->stream));
+    if (c) CK(cudaFreeAsync(c, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+extern "C" int svr_get_stats(svr_volume* v, svr_stats* out) {
+    VOL_CHECK(v);
+    if (!out) return fail(SVR_E_INVALID, "out is NULL");
+    ull h[kStCount];
+    CK(cudaMemcpyAsync(h, v->d_stats, sizeof h, cudaMemcpyDeviceToHost, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    out->frames_inserted = v->frames;
+    out->pixels_inserted = h[kStInserted];
+    out->pixels_oob = h[kStOob];
+    out->pixels_skipped_zero = h[kStSkipped];
+    out->pixels_saturated = h[kStSaturated];
+    out->exact_fallbacks = h[kStFallback];
+    out->kernel_launches = v->launches;
+    return SVR_OK;
+}
+
+extern "C" int svr_count_footprint(svr_volume* v, const uint8_t* px, int64_t pitch, int64_t fstride,
+                                   int32_t w, int32_t h, int32_t n, const svr_rigid* poses,
+                                   const svr_calib* c, int32_t skip_zero, int64_t* distinct) {
+    VOL_CHECK(v);
+    if (!distinct) return fail(SVR_E_INVALID, "distinct_out is NULL");
+    if (n <= 0) return SVR_OK;
+    uint32_t* mark = nullptr;
+    ull* cnt = nullptr;
+    CK(cudaMallocAsync(&mark, sizeof(uint32_t) * v->nvox, v->stream));
+    CK(cudaMemsetAsync(mark, 0, sizeof(uint32_t) * v->nvox, v->stream));
+    CK(cudaMallocAsync(&cnt, sizeof(ull) * n, v->stream));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(ull) * n, v->stream));
+    int rc = SVR_OK;
+    // one frame per launch: the tag (frame index + 1) identifies "already counted this frame"
+    for (int k = 0; k < n && rc == SVR_OK; ++k)
+        rc = insert_common(v, kModeFootprint, px + (long long)k * fstride, pitch, fstride, w, h, 1,
+                           poses + k, c, skip_zero, false, mark, (uint32_t)k + 1u, cnt + k);
+    std::vector<ull> hc(n);
+    if (rc == SVR_OK) {
+        CK(cudaMemcpyAsync(hc.data(), cnt, sizeof(ull) * n, cudaMemcpyDeviceToHost, v->stream));
+        CK(cudaStreamSynchronize(v->stream));
+        for (int k = 0; k < n; ++k) distinct[k] = (int64_t)hc[k];
+    }
+    cudaFreeAsync(mark, v->stream);
+    cudaFreeAsync(cnt, v->stream);
+    cudaStreamSynchronize(v->stream);
+    return rc;
+}
+
+extern "C" int svr_synth_frames(void* dst, int32_t w, int32_t h, int32_t first, int32_t n,
+                                const svr_calib* c, const svr_rigid* poses, int32_t kind, uint64_t seed,
+                                int device, void* stream) {
+    if (!dst || !c || !poses || n <= 0 || w <= 0 || h <= 0) return fail(SVR_E_INVALID, "bad synth arguments");
+    if (n > 65535) return fail(SVR_E_INVALID, "synth at most 65535 frames per call");
+    CK(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    svr_rigid* dp = nullptr;
+    CK(cudaMallocAsync(&dp, sizeof(svr_rigid) * n, s));
+    CK(cudaMemcpyAsync(dp, poses, sizeof(svr_rigid) * n, cudaMemcpyHostToDevice, s));
+    const long long px = (long long)w * h;
+    dim3 grd((unsigned)std::min<long long>((px + 255) / 256, 1024), n);
+    k_synth<<<grd, 256, 0, s>>>((uint8_t*)dst, w, h, first, dev_calib(*c), dp, kind, (ull)seed);
+    CKL();
+    CK(cudaFreeAsync(dp, s));
+    CK(cudaStreamSynchronize(s));
+    return SVR_OK;
+}

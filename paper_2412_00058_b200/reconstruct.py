@@ -1,0 +1,314 @@
+"""Host-side mirror of the reference `reconstruct` / `project` interface (SPEC.md:271-351,
+SPEC.md:452-511) over the C-ABI.  Same operation names, argument meaning and error
+behaviour (InvalidInput / AlgorithmFailure / IoError, core.hpp:14-32); every operation runs
+on the GPU through libspinevol_b200.so — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from typing import Iterable, Optional
+
+import numpy as np
+
+from . import _abi
+from ._abi import (Box, Calib, GridDesc, InvalidInput, Rigid, RenderParams, check, lib, ptr,
+                   rigid_array, rigid_ptr)
+
+EMPTY_BOX = (1, 1, 1, 0, 0, 0)
+
+
+def _box(b) -> Optional[Box]:
+    if b is None:
+        return None
+    if isinstance(b, Box):
+        return b
+    return Box(*[int(v) for v in b])
+
+
+def _frames_view(frames):
+    """(pointer, row_pitch, frame_stride, n, h, w) for a (h,w) or (n,h,w) u8 array/tensor."""
+    if isinstance(frames, np.ndarray):
+        if frames.dtype != np.uint8:
+            raise InvalidInput("frames must be uint8")
+        a = frames if frames.ndim == 3 else frames[None]
+        if a.ndim != 3:
+            raise InvalidInput("frames must be (h,w) or (n,h,w)")
+        if a.strides[2] != 1:
+            a = np.ascontiguousarray(a)
+        n, h, w = a.shape
+        return a, a.ctypes.data, a.strides[1], a.strides[0], n, h, w
+    # torch tensor (host or device)
+    t = frames if frames.dim() == 3 else frames.unsqueeze(0)
+    if str(t.dtype) != "torch.uint8":
+        raise InvalidInput("frames must be uint8")
+    if t.stride(2) != 1:
+        t = t.contiguous()
+    n, h, w = t.shape
+    return t, t.data_ptr(), t.stride(1), t.stride(0), n, h, w
+
+
+class VoxelGrid:
+    """VoxelGrid: u32 sum + u16 count per voxel (packed on the device as one
+    64-bit word), x-fastest layout.  `z_range` selects the stored slab."""
+
+    def __init__(self, dims, voxel_mm: float = 1.0, origin=(0.0, 0.0, 0.0), device: int = 0,
+                 z_range=None, accum: int = _abi.ACC_PNN):
+        d = GridDesc()
+        d.nx, d.ny, d.nz = (int(v) for v in dims)
+        d.accum = accum
+        d.voxel_mm = float(voxel_mm)
+        for k in range(3):
+            d.origin_mm[k] = float(origin[k])
+        d.z_begin, d.z_end = (0, d.nz) if z_range is None else (int(z_range[0]), int(z_range[1]))
+        self.desc = d
+        self.device = device
+        h = C.c_void_p()
+        check(lib().svr_create(C.byref(d), device, C.byref(h)))
+        self._h = h
+        self.insert_seconds = []
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().svr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def dims(self):
+        return (self.desc.nx, self.desc.ny, self.desc.nz)
+
+    @property
+    def slab(self):
+        return (self.desc.z_begin, self.desc.z_end)
+
+    def set_stream(self, cuda_stream: int | None):
+        check(lib().svr_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
+
+    def clear(self):
+        check(lib().svr_clear(self._h))
+
+    def sync(self):
+        check(lib().svr_sync(self._h))
+
+    # -- reconstruct
+    def insert_frame(self, frame, pose, calib: Calib, skip_zero: bool = False) -> Box:
+        """insert_frame; returns the tight DirtyRegion."""
+        keep, p, pitch, _, n, h, w = _frames_view(frame)
+        if n != 1:
+            raise InvalidInput("insert_frame takes one frame")
+        pa = rigid_array(pose)
+        b = Box()
+        check(lib().svr_insert_frame(self._h, p, pitch, w, h, rigid_ptr(pa), C.byref(calib),
+                                     int(skip_zero), C.byref(b)))
+        return b
+
+    def insert_frames(self, frames, poses, calib: Calib, skip_zero: bool = False,
+                      want_boxes: bool = False):
+        """Batched insert.  want_boxes=True returns (per-frame boxes, union box) and syncs;
+        otherwise the call is asynchronous on the grid's stream and returns None."""
+        keep, p, pitch, stride, n, h, w = _frames_view(frames)
+        pa = rigid_array(poses)
+        if len(pa) != n:
+            raise InvalidInput("need one pose per frame")
+        if want_boxes:
+            boxes = (Box * max(n, 1))()
+            u = Box()
+            check(lib().svr_insert_frames(self._h, p, pitch, stride, w, h, n, rigid_ptr(pa),
+                                          C.byref(calib), int(skip_zero), boxes, C.byref(u)))
+            return [boxes[i] for i in range(n)], u
+        check(lib().svr_insert_frames(self._h, p, pitch, stride, w, h, n, rigid_ptr(pa),
+                                      C.byref(calib), int(skip_zero), None, None))
+        return None
+
+    def fill_holes(self, region=None, radius: int = 1, mode: int = _abi.FILL_MEAN,
+                   count: bool = True) -> Optional[int]:
+        """fill_holes over exactly `region` (None = whole slab)."""
+        out = C.c_int64(0)
+        check(lib().svr_fill_holes(self._h, C.byref(_box(region)) if region is not None else None,
+                                   mode, radius, C.byref(out) if count else None))
+        return int(out.value) if count else None
+
+    # -- project
+    def render_coronal(self, dirty=None, params: RenderParams = None, fill_radius: int = 1):
+        from .synth import render_params
+        params = params or render_params()
+        check(lib().svr_render_coronal(self._h, C.byref(_box(dirty)) if dirty is not None else None,
+                                       fill_radius, C.byref(params)))
+
+    def read_coronal(self, z0=None, z1=None):
+        z0 = self.desc.z_begin if z0 is None else z0
+        z1 = self.desc.z_end - 1 if z1 is None else z1
+        n = (z1 - z0 + 1) * self.desc.nx
+        mean = np.empty(n, np.float32)
+        mx = np.empty(n, np.float32)
+        dep = np.empty(n, np.int32)
+        check(lib().svr_read_coronal(self._h, z0, z1, ptr(mean), ptr(mx), ptr(dep)))
+        shp = (z1 - z0 + 1, self.desc.nx)
+        return mean.reshape(shp), mx.reshape(shp), dep.reshape(shp)
+
+    def read_coronal_into(self, z0, z1, mean, mx, depth=None):
+        """Copy rendered rows into caller buffers (host or device, e.g. torch tensors)."""
+        check(lib().svr_read_coronal(self._h, z0, z1, ptr(mean), ptr(mx), ptr(depth)))
+
+    def coronal_projection(self, mode: int = _abi.PROJ_MAX, depth_axis: int = 2,
+                           use_fills: bool = False) -> np.ndarray:
+        """coronal_projection: u8 image over the two remaining axes."""
+        dims = [self.desc.nx, self.desc.ny, self.desc.z_end - self.desc.z_begin]
+        rest = [dims[a] for a in range(3) if a != depth_axis]
+        out = np.empty(rest[0] * rest[1], np.uint8)
+        check(lib().svr_coronal_projection(self._h, mode, depth_axis, int(use_fills), ptr(out)))
+        return out.reshape(rest[1], rest[0])
+
+    # -- readout
+    def _box_shape(self, box):
+        b = _box(box) if box is not None else Box(0, 0, self.desc.z_begin, self.desc.nx - 1,
+                                                  self.desc.ny - 1, self.desc.z_end - 1)
+        return b, (b.z1 - b.z0 + 1, b.y1 - b.y0 + 1, b.x1 - b.x0 + 1)
+
+    def accumulators(self, box=None):
+        b, shp = self._box_shape(box)
+        s = np.empty(shp, np.uint32)
+        c = np.empty(shp, np.uint16)
+        check(lib().svr_read_accumulators(self._h, C.byref(b), ptr(s), ptr(c)))
+        return s, c
+
+    def values(self, box=None, apply_fills=False):
+        """VoxelGrid::value = round(sum/count), 0 when empty."""
+        b, shp = self._box_shape(box)
+        out = np.empty(shp, np.uint8)
+        check(lib().svr_read_values(self._h, C.byref(b), int(apply_fills), ptr(out)))
+        return out
+
+    def fill_layer(self, box=None):
+        b, shp = self._box_shape(box)
+        out = np.empty(shp, np.uint32)
+        check(lib().svr_read_fill(self._h, C.byref(b), ptr(out)))
+        return out
+
+    def trilinear(self, box=None):
+        b, shp = self._box_shape(box)
+        ws = np.empty(shp, np.float32)
+        wt = np.empty(shp, np.float32)
+        check(lib().svr_read_trilinear(self._h, C.byref(b), ptr(ws), ptr(wt)))
+        return ws, wt
+
+    def stats(self) -> dict:
+        s = _abi.Stats()
+        check(lib().svr_get_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def footprint(self, frames, poses, calib, skip_zero=False) -> np.ndarray:
+        keep, p, pitch, stride, n, h, w = _frames_view(frames)
+        pa = rigid_array(poses)
+        out = np.zeros(n, np.int64)
+        check(lib().svr_count_footprint(self._h, p, pitch, stride, w, h, n, rigid_ptr(pa),
+                                        C.byref(calib), int(skip_zero),
+                                        out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+
+# ------------------------------------------------------------------ SPEC free functions
+def insert_frame(grid: VoxelGrid, frame, pose, calib: Calib, skip_zero: bool = False) -> Box:
+    return grid.insert_frame(frame, pose, calib, skip_zero)
+
+
+def fill_holes(grid: VoxelGrid, region, radius: int = 2, mode: int = _abi.FILL_MEDIAN) -> int:
+    """SPEC default: lower median over Chebyshev radius 2."""
+    return grid.fill_holes(region, radius, mode)
+
+
+def coronal_projection(grid: VoxelGrid, mode: int = _abi.PROJ_MAX, depth_axis: int = 2):
+    return grid.coronal_projection(mode, depth_axis)
+
+
+def frame_bounds(desc: GridDesc, calib: Calib, pose) -> Box:
+    """Conservative voxel box a frame can touch (host only)."""
+    pa = rigid_array(pose)
+    b = Box()
+    check(lib().svr_frame_bounds(C.byref(desc), C.byref(calib), rigid_ptr(pa), C.byref(b)))
+    return b
+
+
+def dilate(b: Box, r: int) -> Box:
+    if b.empty():
+        return b
+    return Box(b.x0 - r, b.y0 - r, b.z0 - r, b.x1 + r, b.y1 + r, b.z1 + r)
+
+
+def run_incremental(frames: Iterable, poses, calib: Calib, grid: VoxelGrid, hole_radius: int = 1,
+                    fill_mode: int = _abi.FILL_MEAN, render: Optional[RenderParams] = None,
+                    skip_zero: bool = False):
+    """run_incremental: per frame insert -> fill(dirty (+) r) -> render.
+    The dirty region used for fill/render is the host-computed conservative frame box, a
+    superset of the tight box, so no device round trip is needed per frame; the result is
+    bit-identical to batch processing.  Returns (grid, stats) with per-frame wall latency
+    percentiles (percentile as core.hpp:101-107)."""
+    pa = rigid_array(poses)
+    lat = []
+    for k, fr in enumerate(frames):
+        t0 = time.perf_counter()
+        grid.insert_frames(fr, pa[k:k + 1], calib, skip_zero)
+        b = frame_bounds(grid.desc, calib, pa[k:k + 1])
+        if not b.empty():
+            grid.fill_holes(dilate(b, hole_radius), hole_radius, fill_mode, count=False)
+            if render is not None:
+                grid.render_coronal(b, render, hole_radius)
+        grid.sync()
+        lat.append((time.perf_counter() - t0) * 1e3)
+    st = grid.stats()
+    if lat:
+        st.update(latency_ms_p50=_percentile(lat, 0.5), latency_ms_p95=_percentile(lat, 0.95),
+                  latency_ms_max=max(lat))
+    return grid, st
+
+
+def _percentile(v, p):
+    s = sorted(v)
+    k = int(p * (len(s) - 1) + 0.5)
+    return s[k]
+
+
+def pose_from_matrix4(m) -> Rigid:
+    """RigidTransform::from_matrix4 (geometry.hpp:245-251)."""
+    a = (C.c_double * 16)(*[float(x) for x in np.asarray(m, dtype=np.float64).reshape(16)])
+    r = Rigid()
+    check(lib().svr_pose_from_matrix4(a, C.byref(r)))
+    return r
+
+
+def compose(a: Rigid, b: Rigid) -> Rigid:
+    r = Rigid()
+    check(lib().svr_compose(C.byref(a), C.byref(b), C.byref(r)))
+    return r
+
+
+def interpolate_pose(t_ms, poses, t: float) -> Rigid:
+    tt = np.ascontiguousarray(t_ms, dtype=np.float64)
+    pa = rigid_array(poses)
+    r = Rigid()
+    check(lib().svr_interpolate_pose(tt.ctypes.data_as(C.POINTER(C.c_double)), rigid_ptr(pa),
+                                     len(pa), float(t), C.byref(r)))
+    return r
+
+
+def pixel_to_world(col, row, calib: Calib, pose: Rigid):
+    out = (C.c_double * 3)()
+    check(lib().svr_pixel_to_world(float(col), float(row), C.byref(calib), C.byref(pose), out))
+    return (out[0], out[1], out[2])

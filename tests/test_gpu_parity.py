@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on seeded inputs.
+Integer outputs (sum, count, dirty boxes, fill layer, depths, u8 projections) must be
+bit-exact; rendered floats within 1e-5 relative (north_star), trilinear f32 within the
+tolerance stated in test_trilinear_tolerance."""
+import numpy as np
+import pytest
+
+import paper_2412_00058_b200 as pkg
+from oracle import oracle as O
+from paper_2412_00058_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _grid(wl, **kw):
+    return pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, device=0, accum=wl.accum, **kw)
+
+
+def _assert_acc(grid, ref):
+    s, c = grid.accumulators()
+    bad = np.argwhere(c != ref.count)
+    assert np.array_equal(c, ref.count), "count mismatch at %d voxels, first %s" % (len(bad), bad[:5])
+    assert np.array_equal(s, ref.sum), "sum mismatch"
+
+
+def test_cfg1_batch_bitexact():
+    wl = synth.cfg1()
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    boxes, union = grid.insert_frames(frames, wl.poses, wl.calib, want_boxes=True)
+    ref = O.OracleGrid.for_workload(wl)
+    rboxes = ref.insert_frames(frames, wl.poses, wl.calib)
+    _assert_acc(grid, ref)
+    assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
+    st = grid.stats()
+    assert st["pixels_inserted"] == ref.stats["inserted"]
+    assert st["pixels_oob"] == ref.stats["oob"]
+    assert st["frames_inserted"] == wl.nframes
+
+
+def test_cfg1_fill_and_render_bitexact():
+    wl = synth.cfg1()
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    _, union = grid.insert_frames(frames, wl.poses, wl.calib, want_boxes=True)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames(frames, wl.poses, wl.calib)
+    region = pkg.dilate(union, 1)
+    n_gpu = grid.fill_holes(region, 1, pkg.FILL_MEAN)
+    n_ref = ref.fill_holes(region, 0, 1)
+    assert n_gpu == n_ref
+    assert np.array_equal(grid.fill_layer(), ref.fill)
+    rp = synth.render_params()
+    grid.render_coronal(None, rp, 1)
+    mean, mx, dep = grid.read_coronal()
+    rmean, rmx, rdep = ref.render(rp)
+    assert np.array_equal(dep, rdep)
+    np.testing.assert_allclose(mean, rmean, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(mx, rmx, rtol=1e-5, atol=0)
+    assert np.array_equal(mean, rmean) and np.array_equal(mx, rmx)  # exact by construction
+
+
+def test_single_frame_api_boxes():
+    wl = synth.small_linear()
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    ref = O.OracleGrid.for_workload(wl)
+    for k in range(wl.nframes):
+        b = grid.insert_frame(frames[k], wl.poses[k:k + 1], wl.calib)
+        rb = ref.insert_frame(frames[k], wl.poses[k:k + 1], wl.calib)
+        assert b.as_tuple() == rb.as_tuple()
+    _assert_acc(grid, ref)
+
+
+@pytest.mark.parametrize("w,h", [(61, 47), (64, 48), (17, 5)])
+@pytest.mark.parametrize("skip_zero", [False, True])
+def test_ragged_and_skip_zero(w, h, skip_zero):
+    wl = synth.small_linear(w=w, h=h, nframes=6)
+    frames = wl.frames_np()
+    frames[:, ::3, ::2] = 0  # zeros for skip_zero
+    grid = _grid(wl)
+    grid.insert_frames(frames, wl.poses, wl.calib, skip_zero=skip_zero)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames(frames, wl.poses, wl.calib, skip_zero=skip_zero)
+    _assert_acc(grid, ref)
+    st = grid.stats()
+    assert st["pixels_skipped_zero"] == ref.stats["skipped_zero"]
+    assert st["pixels_oob"] == ref.stats["oob"]
+
+
+def test_host_pinned_device_pitch_inputs():
+    import torch
+    wl = synth.small_linear(w=64, h=48, nframes=8)
+    frames = wl.frames_np()
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames(frames, wl.poses, wl.calib)
+    padded = np.zeros((wl.nframes, wl.h, 80), np.uint8)
+    padded[:, :, :64] = frames
+    for src in (frames, torch.from_numpy(frames).pin_memory(), torch.from_numpy(frames).cuda(),
+                padded[:, :, :64]):
+        grid = _grid(wl)
+        grid.insert_frames(src, wl.poses, wl.calib)
+        _assert_acc(grid, ref)
+        grid.close()
+
+
+def test_fan_bitexact():
+    wl = synth.small_fan()
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    boxes, _ = grid.insert_frames(frames, wl.poses, wl.calib, want_boxes=True)
+    ref = O.OracleGrid.for_workload(wl)
+    rboxes = ref.insert_frames(frames, wl.poses, wl.calib)
+    _assert_acc(grid, ref)
+    assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
+
+
+def test_cfg3_fan_subset_bitexact():
+    wl = synth.cfg3()
+    idx = np.arange(0, wl.nframes, 45)  # 40 frames spread over the sweep
+    frames = synth.synth_frames_np(wl, 0, 1)  # generator check only
+    frames = np.stack([wl.frames_np(int(k), 1)[0] for k in idx])
+    poses = wl.poses[idx]
+    grid = _grid(wl)
+    grid.insert_frames(frames, poses, wl.calib)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames_mt(frames, poses, wl.calib)
+    _assert_acc(grid, ref)
+
+
+def test_cfg2_subset_bitexact():
+    wl = synth.cfg2()
+    idx = np.concatenate([np.arange(0, 40), np.arange(1200, 1240), np.arange(2360, 2400)])
+    frames = np.stack([wl.frames_np(int(k), 1)[0] for k in idx])
+    poses = wl.poses[idx]
+    grid = _grid(wl)
+    grid.insert_frames(frames, poses, wl.calib)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames_mt(frames, poses, wl.calib)
+    _assert_acc(grid, ref)
+    st = grid.stats()
+    assert st["pixels_inserted"] + st["pixels_oob"] == len(idx) * wl.w * wl.h
+
+
+def test_median_fill_r2_bitexact():
+    wl = synth.small_linear(nframes=6)
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    grid.insert_frames(frames, wl.poses, wl.calib)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames(frames, wl.poses, wl.calib)
+    for mode, r in ((pkg.FILL_MEDIAN, 2), (pkg.FILL_MEDIAN, 1), (pkg.FILL_MEAN, 2), (pkg.FILL_MEDIAN, 3)):
+        n = grid.fill_holes(None, r, mode)
+        nr = ref.fill_holes(None, mode, r)
+        assert n == nr, (mode, r)
+        assert np.array_equal(grid.fill_layer(), ref.fill), (mode, r)
+
+
+def test_incremental_equals_batch():
+    wl = synth.cfg1(nframes=60)
+    frames = wl.frames_np()
+    rp = synth.render_params()
+    inc = _grid(wl)
+    pkg.run_incremental(frames, wl.poses, wl.calib, inc, 1, pkg.FILL_MEAN, render=rp)
+    bat = _grid(wl)
+    _, union = bat.insert_frames(frames, wl.poses, wl.calib, want_boxes=True)
+    bat.fill_holes(pkg.dilate(union, 1), 1, pkg.FILL_MEAN)
+    bat.render_coronal(None, rp, 1)
+    for a, b in zip(inc.accumulators(), bat.accumulators()):
+        assert np.array_equal(a, b)
+    assert np.array_equal(inc.fill_layer(), bat.fill_layer())
+    for a, b in zip(inc.read_coronal(), bat.read_coronal()):
+        assert np.array_equal(a, b)
+
+
+def test_order_independence():
+    wl = synth.cfg1(nframes=50)
+    frames = wl.frames_np()
+    a = _grid(wl)
+    a.insert_frames(frames, wl.poses, wl.calib)
+    perm = np.random.default_rng(0).permutation(wl.nframes)
+    b = _grid(wl)
+    b.insert_frames(frames[perm], wl.poses[perm], wl.calib)
+    for x, y in zip(a.accumulators(), b.accumulators()):
+        assert np.array_equal(x, y)
+
+
+def test_projection_u8():
+    wl = synth.small_linear()
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    grid.insert_frames(frames, wl.poses, wl.calib)
+    grid.fill_holes(None, 1, pkg.FILL_MEAN)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames(frames, wl.poses, wl.calib)
+    ref.fill_holes(None, 0, 1)
+    for mode in (pkg.PROJ_MAX, pkg.PROJ_MEAN):
+        for axis in (0, 1, 2):
+            for uf in (False, True):
+                assert np.array_equal(grid.coronal_projection(mode, axis, uf),
+                                      ref.coronal_projection(mode, axis, uf)), (mode, axis, uf)
+    assert np.array_equal(grid.values(), ref.values())
+    assert np.array_equal(grid.values(apply_fills=True), ref.values(True))
+
+
+def test_trilinear_tolerance():
+    import dataclasses
+    wl = dataclasses.replace(synth.cfg5(nframes=6, dims=(160, 120, 40)), origin=(70.0, 20.0, 9.5))
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    grid.insert_frames(frames, wl.poses, wl.calib)
+    ref = O.OracleGrid.for_workload(wl)
+    for k in range(wl.nframes):
+        ref.insert_trilinear(frames[k], wl.poses[k:k + 1], wl.calib)
+    ws, wt = grid.trilinear()
+    # f32 atomics (order) + 32.32 fixed-point weights: |d| <= 1e-5 |ref| + 1e-4 absolute
+    np.testing.assert_allclose(wt, ref.weight, rtol=1e-5, atol=1e-4)
+    np.testing.assert_allclose(ws, ref.wsum, rtol=1e-5, atol=3e-2)
+
+
+def test_footprint_counts():
+    wl = synth.small_linear(nframes=5)
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    u = grid.footprint(frames, wl.poses, wl.calib)
+    for k in range(wl.nframes):
+        r = O.OracleGrid.for_workload(wl)
+        r.insert_frame(frames[k], wl.poses[k:k + 1], wl.calib)
+        assert u[k] == int((r.count > 0).sum())
