@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -81,6 +82,9 @@ struct svr_volume {
     double fan_angle = 0.0;
     uint64_t launches = 0;
     uint64_t frames = 0;
+    int insert_kernel = 1;      // SVR_INSERT_KERNEL: 1 direct (default), 0 rows, 2 tile
+    int dbg_sink = 0;           // SVR_DEBUG_SINK (experiments): 1 no-op sink, 2 scattered
+    bool dbg_perm = false;      // SVR_DEBUG_PERM=1: strided frame order in the direct kernel
 };
 
 // ---------------------------------------------------------------- host geometry (exact)
@@ -180,24 +184,6 @@ static long long to_fixed(long double x, bool* ok) {
     return std::llroundl(s);
 }
 
-static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid_desc& g,
-                       FrameParams* fp) {
-    if (!finite_rigid(pose)) return fail(SVR_E_INVALID, "pose not finite");
-    Affine a = frame_affine(pose, c, g);
-    bool ok = true;
-    for (int k = 0; k < 3; ++k) {
-        if (!(std::fabs(a.K[k]) < 1.0e8L)) ok = false;
-        fp->A[k] = to_fixed(a.K[k] + 0.5L, &ok);
-        fp->Dc[k] = to_fixed(a.Mv[3 * k] * (long double)c.scale_x_mm, &ok);
-        fp->Dr[k] = to_fixed(a.Mv[3 * k + 1] * (long double)c.scale_y_mm, &ok);
-        fp->K[k] = (double)a.K[k];
-        for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = (double)a.Mv[3 * k + j];
-    }
-    if (!ok) return fail(SVR_E_INVALID, "pose maps the frame too far from the grid (|u| >= 1e8 voxels)");
-    fp->pose = pose;
-    return SVR_OK;
-}
-
 static DevCalib dev_calib(const svr_calib& c) {
     DevCalib d{};
     d.sx = c.scale_x_mm;
@@ -221,6 +207,26 @@ static GridDev dev_grid(const svr_grid_desc& d) {
     g.voxel = d.voxel_mm;
     for (int k = 0; k < 3; ++k) g.o[k] = d.origin_mm[k];
     return g;
+}
+
+static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid_desc& g,
+                       FrameParams* fp) {
+    if (!finite_rigid(pose)) return fail(SVR_E_INVALID, "pose not finite");
+    Affine a = frame_affine(pose, c, g);
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) {
+        if (!(std::fabs(a.K[k]) < 1.0e8L)) ok = false;
+        fp->A[k] = to_fixed(a.K[k] + 0.5L, &ok);
+        fp->Dc[k] = to_fixed(a.Mv[3 * k] * (long double)c.scale_x_mm, &ok);
+        fp->Dr[k] = to_fixed(a.Mv[3 * k + 1] * (long double)c.scale_y_mm, &ok);
+        fp->K[k] = (double)a.K[k];
+        for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = (double)a.Mv[3 * k + j];
+    }
+    if (!ok) return fail(SVR_E_INVALID, "pose maps the frame too far from the grid (|u| >= 1e8 voxels)");
+    fp->pose = pose;
+    fp->cal = dev_calib(c);
+    fp->g = dev_grid(g);
+    return SVR_OK;
 }
 
 // Conservative box (global indices) a frame can touch: affine extremes at the image corners
@@ -510,6 +516,10 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     if (device < 0 || device >= ndev) return fail(SVR_E_INVALID, "device %d out of range", device);
     svr_volume* v = new svr_volume();
     v->d = *desc;
+    if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
+        v->insert_kernel = !std::strcmp(e, "rows") ? 0 : !std::strcmp(e, "tile") ? 2 : 1;
+    if (const char* e = std::getenv("SVR_DEBUG_SINK")) v->dbg_sink = std::atoi(e);
+    if (const char* e = std::getenv("SVR_DEBUG_PERM")) v->dbg_perm = e[0] == '1';
     v->device = device;
     auto bail = [&](int code) {
         svr_destroy(v);
@@ -657,6 +667,14 @@ __global__ void k_box_init(int* b, int n) {
     }
 }
 
+static long long coprime_stride(int n) {
+    if (n <= 2) return 1;
+    long long p = std::max(1ll, (long long)std::llround(n * 0.3819660112501051));
+    auto gcd = [](long long a, long long b) { while (b) { long long t = a % b; a = b; b = t; } return a; };
+    while (gcd(p, n) != 1) ++p;
+    return p;
+}
+
 template <int kMode, bool kVec, bool kSkip, bool kBox>
 static void launch_insert_t(svr_volume* v, const uint8_t* px, long long pitch, long long fstride,
                             int w, int h, int n, const FrameParams* fps, const DevCalib& cal,
@@ -666,7 +684,7 @@ static void launch_insert_t(svr_volume* v, const uint8_t* px, long long pitch, l
     dim3 block(256), grid((chunks + 255) / 256, n);
     k_insert<kMode, kVec, kSkip, kBox><<<grid, block, 0, v->stream>>>(
         px, pitch, fstride, w, h, cpr, fps, cal, v->d_fan, dev_grid(v->d), v->acc, v->tri, mark,
-        tag, boxes, stats);
+        tag, boxes, stats, v->dbg_sink, v->dbg_perm ? coprime_stride(n) : 1);
     v->launches++;
 }
 
@@ -699,25 +717,106 @@ static bool is_device_ptr(const void* p, bool* pinned) {
     return false;
 }
 
+// Tile-hash insert (k_pnn_tile) applicability for a launch: the packed (count<<20 | sum) slot
+// must not overflow (some pixel pair of every tile lies more than a voxel diagonal apart, so no
+// voxel collects all 4096 pixels of a tile) and tile-local keys must fit 32 bits.
+struct TileShape {
+    int tw, th, ntx, nty;
+};
+
+static bool tile_ok(const svr_volume* v, const DevCalib& cal, int w, int h, TileShape* ts) {
+    const int cpr = (w + kChunk - 1) / kChunk;
+    ts->tw = std::min(8, cpr);
+    while (256 % ts->tw) --ts->tw;
+    ts->th = 256 / ts->tw;
+    ts->ntx = (cpr + ts->tw - 1) / ts->tw;
+    ts->nty = (h + ts->th - 1) / ts->th;
+    const double diag = std::sqrt(3.0) * v->d.voxel_mm;
+    const double along = (cal.probe == SVR_PROBE_FAN) ? cal.dr : cal.sx;
+    const double across = (cal.probe == SVR_PROBE_FAN) ? 0.0 : cal.sy;
+    const bool spread = (std::min(ts->tw * kChunk, w) - 1) * along > diag ||
+                        (std::min(ts->th, h) - 1) * across > diag;
+    // keys: a tile spans at most its frame's z extent; bound by the slab (conservative)
+    const double slab = (double)v->d.nx * v->d.ny * (double)(v->d.z_end - v->d.z_begin);
+    return spread && slab < 4.0e9;
+}
+
+template <bool kVec, bool kSkip, bool kBox>
+static void launch_tile_t(svr_volume* v, const uint8_t* px, long long pitch, long long fstride,
+                          int w, int h, int n, const FrameParams* fps, const DevCalib& cal,
+                          const TileShape& ts, int* boxes, ull* stats) {
+    const int cpr = (w + kChunk - 1) / kChunk;
+    dim3 grid(ts.ntx * ts.nty, n);
+    k_pnn_tile<kVec, kSkip, kBox><<<grid, 256, 0, v->stream>>>(
+        px, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, n, coprime_stride(n), fps, cal,
+        v->d_fan, dev_grid(v->d), v->acc, boxes, stats);
+    v->launches++;
+}
+
+static void launch_tile(svr_volume* v, bool vec, bool skip, bool box, const uint8_t* px,
+                        long long pitch, long long fstride, int w, int h, int n,
+                        const FrameParams* fps, const DevCalib& cal, const TileShape& ts,
+                        int* boxes, ull* stats) {
+#define LT(a, b, c) launch_tile_t<a, b, c>(v, px, pitch, fstride, w, h, n, fps, cal, ts, boxes, stats)
+    if (vec) {
+        if (skip) { if (box) LT(true, true, true); else LT(true, true, false); }
+        else { if (box) LT(true, false, true); else LT(true, false, false); }
+    } else {
+        if (skip) { if (box) LT(false, true, true); else LT(false, true, false); }
+        else { if (box) LT(false, false, true); else LT(false, false, false); }
+    }
+#undef LT
+}
+
+template <bool kVec, bool kBox>
+static void launch_rows_t(svr_volume* v, const uint8_t* px, long long pitch, long long fstride,
+                          int w, int h, int n, const FrameParams* fps, const DevCalib& cal,
+                          int* boxes, ull* stats) {
+    const int cpr = (w + kChunk - 1) / kChunk;
+    const int nstrips = (h + kStripRows - 1) / kStripRows;
+    dim3 grid((nstrips * cpr + 255) / 256, n);
+    k_pnn_rows<kVec, kBox><<<grid, 256, 0, v->stream>>>(px, pitch, fstride, w, h, cpr, nstrips, fps,
+                                                        cal, v->d_fan, dev_grid(v->d), v->acc,
+                                                        boxes, stats);
+    v->launches++;
+}
+
 // Launch over frames resident in device memory, chunked to the grid.y limit.
+//   PNN insert: k_insert direct (default), k_pnn_rows (SVR_INSERT_KERNEL=rows, no skip_zero),
+//   k_pnn_tile (SVR_INSERT_KERNEL=tile, when tile_ok); footprint / trilinear: k_insert.
 static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long pitch,
                          long long fstride, int w, int h, int n, const FrameParams* fps,
                          const DevCalib& cal, bool skip, bool box, int* boxes, uint32_t* mark,
                          uint32_t tag, ull* stats) {
     const bool vec = ((uintptr_t)px % 16 == 0) && (pitch % 16 == 0) && (fstride % 16 == 0) &&
                      (w % kChunk == 0);
+    TileShape ts;
+    const bool tile = mode == kModeInsert && v->insert_kernel == 2 && tile_ok(v, cal, w, h, &ts);
+    const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
         const uint8_t* p = px + (long long)k0 * fstride;
-        if (mode == kModeInsert)
+        int* bx = boxes ? boxes + 6 * k0 : nullptr;
+        if (rows) {
+            if (vec) {
+                if (box) launch_rows_t<true, true>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
+                else launch_rows_t<true, false>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
+            } else {
+                if (box) launch_rows_t<false, true>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
+                else launch_rows_t<false, false>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
+            }
+        } else if (tile) {
+            launch_tile(v, vec, skip, box, p, pitch, fstride, w, h, m, fps + k0, cal, ts, bx, stats);
+        } else if (mode == kModeInsert) {
             launch_insert<kModeInsert>(v, vec, skip, box, p, pitch, fstride, w, h, m, fps + k0, cal,
-                                       mark, tag, boxes ? boxes + 6 * k0 : nullptr, stats);
-        else if (mode == kModeTrilinear)
+                                       mark, tag, bx, stats);
+        } else if (mode == kModeTrilinear) {
             launch_insert<kModeTrilinear>(v, vec, skip, false, p, pitch, fstride, w, h, m, fps + k0,
                                           cal, mark, tag, nullptr, stats);
-        else
+        } else {
             launch_insert<kModeFootprint>(v, vec, skip, false, p, pitch, fstride, w, h, m, fps + k0,
                                           cal, mark, tag, nullptr, stats);
+        }
         CKL();
     }
     return SVR_OK;

@@ -1,0 +1,70 @@
+// Microbenchmark: lane-atomic throughput on B200 for the insert kernel's design choices.
+//   red64_spread   : RED.E.ADD.64 to pseudo-random addresses in a 1 MiB window (L2-resident)
+//   red64_run      : RED.64 where 4 consecutive lanes share an address (run-like)
+//   atoms32_spread : shared-memory atomicAdd (u32) to pseudo-random slots of a 16 KiB table
+//   atoms32_run    : shared atomics, 4 lanes per address
+//   sts32_spread   : plain shared stores, same pattern (LSU reference)
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_atomics tools/ubench_atomics.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned hash32(unsigned x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) kern(unsigned long long* g, int iters, unsigned long long* sink) {
+    __shared__ unsigned s[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) s[i] = 0;
+    __syncthreads();
+    unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned lane = threadIdx.x & 31;
+    for (int it = 0; it < iters; ++it) {
+        unsigned key = (MODE == 1 || MODE == 3) ? hash32((t >> 2) * 977u + it) : hash32(t * 131u + it);
+        if (MODE == 0 || MODE == 1) atomicAdd(&g[key & ((1u << 17) - 1)], 1ull);
+        if (MODE == 2 || MODE == 3) atomicAdd(&s[key & 4095], 1u);
+        if (MODE == 4) s[key & 4095] = key;
+        if (MODE == 5) atomicAdd(&g[(key % 30000u) * 7u % (1u << 17)], 1ull);  // hot 30k-address set
+        if (MODE == 6) atomicAdd(&g[(t >> 3) % 30000u], 1ull);                  // 8 lanes/address
+    }
+    __syncthreads();
+    if (MODE >= 2 && threadIdx.x == 0) sink[blockIdx.x] = s[lane];
+}
+
+template <int MODE>
+float run(const char* name, unsigned long long* g, unsigned long long* sink, int blocks, int iters) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    kern<MODE><<<blocks, 256>>>(g, iters, sink);
+    cudaEventRecord(a);
+    kern<MODE><<<blocks, 256>>>(g, iters, sink);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    double ops = (double)blocks * 256 * iters;
+    printf("%-16s %8.3f ms  %8.1f G lane-ops/s\n", name, ms, ops / ms / 1e6);
+    return ms;
+}
+
+int main() {
+    unsigned long long *g, *sink;
+    cudaMalloc(&g, sizeof(unsigned long long) << 17);
+    cudaMalloc(&sink, sizeof(unsigned long long) << 20);
+    cudaMemset(g, 0, sizeof(unsigned long long) << 17);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int blocks = sms * 8, iters = 512;
+    run<0>("red64_spread", g, sink, blocks, iters);
+    run<1>("red64_run4", g, sink, blocks, iters);
+    run<2>("atoms32_spread", g, sink, blocks, iters);
+    run<3>("atoms32_run4", g, sink, blocks, iters);
+    run<4>("sts32_spread", g, sink, blocks, iters);
+    run<5>("red64_hot30k", g, sink, blocks, iters);
+    run<6>("red64_same8", g, sink, blocks, iters);
+    cudaError_t e = cudaDeviceSynchronize();
+    printf("status %s, SMs %d\n", cudaGetErrorString(e), sms);
+    return e == cudaSuccess ? 0 : 1;
+}
