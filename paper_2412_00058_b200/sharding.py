@@ -1,0 +1,82 @@
+"""z-slab sharding of the volume across ranks (one process per GPU).
+
+Rank r owns global planes [owned_begin, owned_end) and stores [alloc_begin, alloc_end): the
+owned planes plus `ghost` = fill_radius + median_radius planes on each side, so the hole fill
+and the 5x5-median render of every owned column see exactly the voxels the unsharded volume
+would.  A frame is routed to every rank whose stored planes its conservative
+voxel box meets; each rank inserts independently (integer sums, no exchange).  The only
+collective is the gather of the rendered coronal rows (NCCL all-gather over NVLink on GPUs,
+gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+
+
+@dataclass
+class Slab:
+    owned: tuple
+    alloc: tuple
+
+
+def plan_slabs(nz: int, nranks: int, ghost: int):
+    """Contiguous near-equal z-slabs (svr_plan_slabs)."""
+    ob, oe, ab, ae = ((_abi.I32 * nranks)() for _ in range(4))
+    _abi.check(_abi.lib().svr_plan_slabs(nz, nranks, ghost, ob, oe, ab, ae))
+    return [Slab((ob[r], oe[r]), (ab[r], ae[r])) for r in range(nranks)]
+
+
+def frame_boxes(desc: _abi.GridDesc, calib: _abi.Calib, poses) -> list:
+    """Conservative global voxel box of every frame (svr_frame_bounds, host only)."""
+    pa = _abi.rigid_array(poses)
+    out = []
+    for k in range(len(pa)):
+        b = _abi.Box()
+        _abi.check(_abi.lib().svr_frame_bounds(C.byref(desc), C.byref(calib),
+                                               _abi.rigid_ptr(pa[k:k + 1]), C.byref(b)))
+        out.append(b)
+    return out
+
+
+def route(boxes, alloc) -> np.ndarray:
+    """Indices of the frames whose box meets the stored planes [alloc0, alloc1)."""
+    return np.array([k for k, b in enumerate(boxes)
+                     if not b.empty() and b.z1 >= alloc[0] and b.z0 < alloc[1]], dtype=np.int64)
+
+
+def union_box(boxes, idx, alloc) -> _abi.Box:
+    """Union of the routed frames' boxes clipped to the stored planes (empty if none)."""
+    if len(idx) == 0:
+        return _abi.Box(1, 1, 1, 0, 0, 0)
+    bs = [boxes[int(k)] for k in idx]
+    z0 = max(min(b.z0 for b in bs), alloc[0])
+    z1 = min(max(b.z1 for b in bs), alloc[1] - 1)
+    if z0 > z1:
+        return _abi.Box(1, 1, 1, 0, 0, 0)
+    return _abi.Box(min(b.x0 for b in bs), min(b.y0 for b in bs), z0, max(b.x1 for b in bs),
+                    max(b.y1 for b in bs), z1)
+
+
+def gather_rows(local, slab: Slab, slabs, dist):
+    """All-gather each rank's owned coronal rows (torch tensor [owned_rows, ...]) into the full
+    image [nz, ...] (padded equal strips, one all_gather_into_tensor).  Returns the image."""
+    import torch
+    rows_max = max(s.owned[1] - s.owned[0] for s in slabs)
+    world = len(slabs)
+    pad = torch.zeros((rows_max,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    if local.device.type == "cuda":
+        buf = torch.empty((world * rows_max,) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
+        dist.all_gather_into_tensor(buf, pad)
+    else:  # gloo
+        lst = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(lst, pad)
+        buf = torch.cat(lst, 0)
+    parts = [buf[r * rows_max: r * rows_max + (slabs[r].owned[1] - slabs[r].owned[0])] for r in range(world)]
+    return torch.cat(parts, 0)

@@ -227,3 +227,44 @@ def test_footprint_counts():
         r = O.OracleGrid.for_workload(wl)
         r.insert_frame(frames[k], wl.poses[k:k + 1], wl.calib)
         assert u[k] == int((r.count > 0).sum())
+
+
+@pytest.mark.parametrize("name", ["small_linear", "small_fan"])
+@pytest.mark.parametrize("kernel", ["direct", "rows", "tile"])
+def test_golden_fixtures_gpu(name, kernel, monkeypatch):
+    """CUDA path against the committed fixtures (accumulators from the reference's own
+    pixel_to_world, tests/golden/make_golden.py) for every insert kernel variant."""
+    from golden_util import Fixture
+    monkeypatch.setenv("SVR_INSERT_KERNEL", kernel)
+    fx = Fixture(name)
+    grid = pkg.VoxelGrid(fx.dims, fx.voxel_mm, fx.origin, device=0)
+    boxes, _ = grid.insert_frames(fx.frames, fx.poses, fx.calib, want_boxes=True)
+    s, c = grid.accumulators()
+    assert np.array_equal(s, fx["sum"]) and np.array_equal(c, fx["count"])
+    assert np.array_equal(np.array([b.as_tuple() for b in boxes]), fx["boxes"])
+    assert grid.fill_holes(None, 1, pkg.FILL_MEAN) == int(fx["filled_mean_r1"])
+    assert np.array_equal(grid.fill_layer(), fx["fill_mean_r1"])
+    grid.render_coronal(None, fx.render, 1)
+    mean, mx, dep = grid.read_coronal()
+    assert np.array_equal(dep, fx["render_depth"])
+    np.testing.assert_allclose(mean, fx["render_mean"], rtol=1e-5, atol=0)
+    np.testing.assert_allclose(mx, fx["render_max"], rtol=1e-5, atol=0)
+    grid.fill_holes(None, 2, pkg.FILL_MEDIAN)
+    assert np.array_equal(grid.fill_layer(), fx["fill_median_r2"])
+    g0 = pkg.VoxelGrid(fx.dims, fx.voxel_mm, fx.origin, device=0)
+    g0.insert_frames(fx.frames, fx.poses, fx.calib, skip_zero=True)
+    s0, c0 = g0.accumulators()
+    assert np.array_equal(s0, fx["sum_skip0"]) and np.array_equal(c0, fx["count_skip0"])
+
+
+@pytest.mark.parametrize("kernel", ["direct", "rows", "tile"])
+def test_cfg1_all_kernels(kernel, monkeypatch):
+    monkeypatch.setenv("SVR_INSERT_KERNEL", kernel)
+    wl = synth.cfg1()
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    boxes, _ = grid.insert_frames(frames, wl.poses, wl.calib, want_boxes=True)
+    ref = O.OracleGrid.for_workload(wl)
+    rboxes = ref.insert_frames(frames, wl.poses, wl.calib)
+    _assert_acc(grid, ref)
+    assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
