@@ -999,18 +999,18 @@ extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode
     if (any) {
         const GridDev g = dev_grid(v->d);
         const int bx = b.x1 - b.x0 + 1, by = b.y1 - b.y0 + 1, bz = b.z1 - b.z0 + 1;
-        if (radius == 1) {
-            dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 15) / 16);
-            if (mode == SVR_FILL_MEAN)
-                k_fill<1, SVR_FILL_MEAN, 32, 8, 16><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+        if (mode == SVR_FILL_MEAN && radius <= 2) {
+            dim3 grd((bx + 31) / 32, (by + 7) / 8, (bz + 31) / 32);
+            if (radius == 1)
+                k_fill_sep<1><<<grd, dim3(34, 10), 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
             else
-                k_fill<1, SVR_FILL_MEDIAN, 32, 8, 16><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+                k_fill_sep<2><<<grd, dim3(36, 12), 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+        } else if (radius == 1) {
+            dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 15) / 16);
+            k_fill<1, SVR_FILL_MEDIAN, 32, 8, 16><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
         } else if (radius == 2) {
             dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 7) / 8);
-            if (mode == SVR_FILL_MEAN)
-                k_fill<2, SVR_FILL_MEAN, 32, 8, 8><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
-            else
-                k_fill<2, SVR_FILL_MEDIAN, 32, 8, 8><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
+            k_fill<2, SVR_FILL_MEDIAN, 32, 8, 8><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
         } else {
             long long nv = (long long)bx * by * bz;
             k_fill_generic<<<(unsigned)((nv + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, g, b, radius, mode, v->d_counter);
@@ -1194,7 +1194,7 @@ extern "C" int svr_read_fill(svr_volume* v, const svr_box* box, uint32_t* out) {
     if (int e = read_box_common(v, box, &b, &n)) return e;
     uint32_t* t = nullptr;
     CK(cudaMallocAsync(&t, n * 4, v->stream));
-    k_read_box<uint32_t><<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->fill, dev_grid(v->d), b, t);
+    k_read_fill<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, dev_grid(v->d), b, t);
     v->launches++;
     CKL();
     CK(cudaMemcpyAsync(out, t, n * 4, cudaMemcpyDefault, v->stream));
