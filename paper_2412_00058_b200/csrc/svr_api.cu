@@ -82,9 +82,7 @@ struct svr_volume {
     double fan_angle = 0.0;
     uint64_t launches = 0;
     uint64_t frames = 0;
-    int insert_kernel = 1;      // SVR_INSERT_KERNEL: 1 direct (default), 0 rows, 2 tile
-    int dbg_sink = 0;           // SVR_DEBUG_SINK (experiments): 1 no-op sink, 2 scattered
-    bool dbg_perm = false;      // SVR_DEBUG_PERM=1: strided frame order in the direct kernel
+    int insert_kernel = 1;      // SVR_INSERT_KERNEL: 1 direct (default), 3 plane, 0 rows, 2 tile
 };
 
 // ---------------------------------------------------------------- host geometry (exact)
@@ -226,6 +224,11 @@ static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid
     fp->pose = pose;
     fp->cal = dev_calib(c);
     fp->g = dev_grid(g);
+    // image-plane normal in voxel space = third column of R_pose R_calib (k_pnn_plane table)
+    {
+        const long double nx = std::fabs(a.Mv[2]), ny = std::fabs(a.Mv[5]), nz = std::fabs(a.Mv[8]);
+        fp->plane_ok = (nx + ny) < 0.99L * nz ? 1 : 0;
+    }
     return SVR_OK;
 }
 
@@ -517,9 +520,11 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     svr_volume* v = new svr_volume();
     v->d = *desc;
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
-        v->insert_kernel = !std::strcmp(e, "rows") ? 0 : !std::strcmp(e, "tile") ? 2 : 1;
-    if (const char* e = std::getenv("SVR_DEBUG_SINK")) v->dbg_sink = std::atoi(e);
-    if (const char* e = std::getenv("SVR_DEBUG_PERM")) v->dbg_perm = e[0] == '1';
+        v->insert_kernel = !std::strcmp(e, "rows")     ? 0
+                           : !std::strcmp(e, "tile")   ? 2
+                           : !std::strcmp(e, "plane")  ? 3
+                                                       : 1;
+
     v->device = device;
     auto bail = [&](int code) {
         svr_destroy(v);
@@ -684,7 +689,7 @@ static void launch_insert_t(svr_volume* v, const uint8_t* px, long long pitch, l
     dim3 block(256), grid((chunks + 255) / 256, n);
     k_insert<kMode, kVec, kSkip, kBox><<<grid, block, 0, v->stream>>>(
         px, pitch, fstride, w, h, cpr, fps, cal, v->d_fan, dev_grid(v->d), v->acc, v->tri, mark,
-        tag, boxes, stats, v->dbg_sink, v->dbg_perm ? coprime_stride(n) : 1);
+        tag, boxes, stats);
     v->launches++;
 }
 
@@ -782,7 +787,8 @@ static void launch_rows_t(svr_volume* v, const uint8_t* px, long long pitch, lon
 }
 
 // Launch over frames resident in device memory, chunked to the grid.y limit.
-//   PNN insert: k_insert direct (default), k_pnn_rows (SVR_INSERT_KERNEL=rows, no skip_zero),
+//   PNN insert: k_insert direct (default), k_pnn_plane (SVR_INSERT_KERNEL=plane, when tile_ok
+//   and no skip_zero), k_pnn_rows (=rows),
 //   k_pnn_tile (SVR_INSERT_KERNEL=tile, when tile_ok); footprint / trilinear: k_insert.
 static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long pitch,
                          long long fstride, int w, int h, int n, const FrameParams* fps,
@@ -791,13 +797,27 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     const bool vec = ((uintptr_t)px % 16 == 0) && (pitch % 16 == 0) && (fstride % 16 == 0) &&
                      (w % kChunk == 0);
     TileShape ts;
-    const bool tile = mode == kModeInsert && v->insert_kernel == 2 && tile_ok(v, cal, w, h, &ts);
+    const bool tiled = mode == kModeInsert && (v->insert_kernel == 2 || v->insert_kernel == 3) &&
+                       tile_ok(v, cal, w, h, &ts);
+    const bool tile = tiled && v->insert_kernel == 2;
+    const bool plane = tiled && v->insert_kernel == 3 && !skip;
     const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
         const uint8_t* p = px + (long long)k0 * fstride;
         int* bx = boxes ? boxes + 6 * k0 : nullptr;
-        if (rows) {
+        if (plane) {
+            const int cpr = (w + kChunk - 1) / kChunk;
+            dim3 grid(ts.ntx * ts.nty, m);
+            if (vec) {
+                if (box) k_pnn_plane<true, true><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
+                else k_pnn_plane<true, false><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
+            } else {
+                if (box) k_pnn_plane<false, true><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
+                else k_pnn_plane<false, false><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
+            }
+            v->launches++;
+        } else if (rows) {
             if (vec) {
                 if (box) launch_rows_t<true, true>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
                 else launch_rows_t<true, false>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);

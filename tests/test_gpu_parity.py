@@ -230,7 +230,7 @@ def test_footprint_counts():
 
 
 @pytest.mark.parametrize("name", ["small_linear", "small_fan"])
-@pytest.mark.parametrize("kernel", ["direct", "rows", "tile"])
+@pytest.mark.parametrize("kernel", ["plane", "direct", "rows", "tile"])
 def test_golden_fixtures_gpu(name, kernel, monkeypatch):
     """CUDA path against the committed fixtures (accumulators from the reference's own
     pixel_to_world, tests/golden/make_golden.py) for every insert kernel variant."""
@@ -257,7 +257,7 @@ def test_golden_fixtures_gpu(name, kernel, monkeypatch):
     assert np.array_equal(s0, fx["sum_skip0"]) and np.array_equal(c0, fx["count_skip0"])
 
 
-@pytest.mark.parametrize("kernel", ["direct", "rows", "tile"])
+@pytest.mark.parametrize("kernel", ["plane", "direct", "rows", "tile"])
 def test_cfg1_all_kernels(kernel, monkeypatch):
     monkeypatch.setenv("SVR_INSERT_KERNEL", kernel)
     wl = synth.cfg1()
