@@ -183,13 +183,62 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+
+# ---------------------------------------------------------------- secondary configs (N=1)
+def measure_config(name, steps=3):
+    """Insert-only throughput of another BASELINE config on this GPU (device-resident frames):
+    cfg1 (small linear), cfg3 (convex fan), cfg5 (2x2x2 trilinear f32 splat into the full
+    2000x1000x7500 = 15 G-voxel, 120 GB volume)."""
+    import torch
+
+    import paper_2412_00058_b200 as pkg
+    from paper_2412_00058_b200 import _abi, synth
+    wl = synth.CONFIGS[name]()
+    vox = int(np.prod(wl.dims))
+    need = vox * 8 + wl.nframes * wl.w * wl.h
+    free = torch.cuda.mem_get_info()[0]
+    if need > free * 0.95:
+        return {"skipped": "needs %.1f GB, %.1f GB free" % (need / 1e9, free / 1e9)}
+    frames = torch.empty((wl.nframes, wl.h, wl.w), dtype=torch.uint8, device="cuda")
+    synth.synth_frames_device(wl, frames, 0, wl.nframes, torch.cuda.current_device())
+    grid = pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, accum=wl.accum,
+                         device=torch.cuda.current_device())
+    stream = torch.cuda.Stream()
+    grid.set_stream(stream.cuda_stream)
+    out = {"workload": wl.name, "frames": wl.nframes, "frame": [wl.h, wl.w], "grid": list(wl.dims),
+           "voxel_mm": wl.voxel_mm, "accum": "trilinear-f32" if wl.accum == _abi.ACC_TRILINEAR else "pnn-u32"}
+    if wl.accum == _abi.ACC_PNN:
+        U = grid.footprint(frames, wl.poses, wl.calib)
+        grid.clear()
+        alg = float(wl.nframes * wl.w * wl.h + 12 * int(U.sum()))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps + 1)]
+    with torch.cuda.stream(stream):
+        for i in range(steps + 1):
+            ev[i][0].record(stream)
+            grid.insert_frames(frames, wl.poses, wl.calib)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev[1:]) / steps
+    out["insert_ms"] = ms
+    out["value"] = wl.nframes * wl.w * wl.h / (ms / 1e3) / 1e9
+    out["unit"] = UNIT
+    if wl.accum == _abi.ACC_PNN:
+        hbm, _ = _peaks()
+        out["roofline_frac"] = alg / (ms / 1e3) / 1e9 / hbm
+        out["U_mean"] = float(U.mean())
+    grid.close()
+    del frames
+    torch.cuda.empty_cache()
+    return out
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2412_00058_b200 as pkg
-    from paper_2412_00058_b200 import _abi, synth
+    from paper_2412_00058_b200 import _abi, sharding, synth
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -214,34 +263,27 @@ def run_ours(args):
     fill_r, med_r = wl.fill_radius, synth.CFG4_RENDER["median_radius"]
     ghost = fill_r + med_r
     nz = wl.dims[2]
-    ob, oe, ab, ae = ((_abi.I32 * world)() for _ in range(4))
-    _abi.check(_abi.lib().svr_plan_slabs(nz, world, ghost, ob, oe, ab, ae))
-    own = (ob[rank], oe[rank])
-    alloc = (ab[rank], ae[rank])
-    desc = wl.grid_desc(*alloc)
+    slabs = sharding.plan_slabs(nz, world, ghost)
+    own, alloc = slabs[rank].owned, slabs[rank].alloc
+    ob = [s_.owned[0] for s_ in slabs]
+    oe = [s_.owned[1] for s_ in slabs]
 
     # frame routing: every frame whose conservative box meets this rank's stored slab
-    boxes = [pkg.frame_bounds(wl.grid_desc(), wl.calib, wl.poses[k:k + 1]) for k in range(wl.nframes)]
-    mine = np.array([k for k, b in enumerate(boxes)
-                     if not b.empty() and b.z1 >= alloc[0] and b.z0 < alloc[1]], dtype=np.int64)
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    mine = sharding.route(boxes, alloc)
     poses = wl.poses[mine]
-    ub = [min(boxes[k].x0 for k in mine), min(boxes[k].y0 for k in mine),
-          max(min(boxes[k].z0 for k in mine), alloc[0]), max(boxes[k].x1 for k in mine),
-          max(boxes[k].y1 for k in mine), min(max(boxes[k].z1 for k in mine), alloc[1] - 1)]
-    union = _abi.Box(*ub)
+    union = sharding.union_box(boxes, mine, alloc)
     fill_region = pkg.dilate(union, fill_r)
     rp = synth.render_params()
 
-    # device-resident frames from the seeded generator
-    k0, k1 = int(mine[0]), int(mine[-1]) + 1
-    span = torch.empty((k1 - k0, wl.h, wl.w), dtype=torch.uint8, device=dev)
-    for a in range(k0, k1, 4096):
-        b = min(k1, a + 4096)
-        _abi.check(_abi.lib().svr_synth_frames(
-            span[a - k0].data_ptr(), wl.w, wl.h, a, b - a, wl.calib,
-            _abi.rigid_ptr(np.ascontiguousarray(wl.poses[a:b])), wl.kind, wl.seed, local, None))
-    frames = span[torch.from_numpy(mine - k0).to(dev)].contiguous() if len(mine) != k1 - k0 else span
-    del span
+    # device-resident frames from the seeded generator (only this rank's frames)
+    frames = torch.empty((len(mine), wl.h, wl.w), dtype=torch.uint8, device=dev)
+    if len(mine):
+        k0, k1 = int(mine[0]), int(mine[-1]) + 1
+        span = torch.empty((k1 - k0, wl.h, wl.w), dtype=torch.uint8, device=dev)
+        synth.synth_frames_device(wl, span, k0, k1 - k0, local)
+        frames = span[torch.from_numpy(mine - k0).to(dev)].contiguous() if len(mine) != k1 - k0 else span
+        del span
     n_my = frames.shape[0]
     px_frame = wl.w * wl.h
     total_px = wl.nframes * px_frame  # units of the whole job
@@ -251,7 +293,7 @@ def run_ours(args):
     grid.set_stream(stream.cuda_stream)
 
     # algorithmic bytes of the insert launch: sum_f (W*H + U_f * 12)
-    U = grid.footprint(frames, poses, wl.calib)
+    U = grid.footprint(frames, poses, wl.calib) if n_my else np.zeros(1, np.int64)
     alg_bytes = float(n_my * px_frame + 12 * int(U.sum()))
     grid.clear()
 
@@ -349,7 +391,7 @@ def run_ours(args):
 
     stats = grid.stats()
     hbm, peak_src = _peaks()
-    ins_s = ins_ms / 1e3
+    ins_s = max(ins_ms, 1e-9) / 1e3
     achieved = alg_bytes / ins_s / 1e9
     value = total_px * args.steps / (elapsed_ms / 1e3) / 1e9
     e2e_value = total_px * e2e_steps / e2e_s / 1e9
@@ -364,6 +406,18 @@ def run_ours(args):
                "sample": "%d of 2400 cfg2 frames (every %dth, %.1f Mpx) x %d passes, PNN insert only, "
                          "%d threads, %s" % (len(idx), args.cpu_every, px / 1e6, len(times), nth,
                                              _cpu_model())}
+
+    others = None
+    if rank == 0 and world == 1 and not args.no_other_configs:
+        grid.close()
+        del frames
+        torch.cuda.empty_cache()
+        others = {}
+        for name in ("cfg1", "cfg3", "cfg5"):
+            try:
+                others[name] = measure_config(name)
+            except Exception as e:  # report, never hide the headline line
+                others[name] = {"error": str(e)[:200]}
 
     def pct(v, p):
         s = sorted(v)
@@ -404,10 +458,12 @@ def run_ours(args):
         "clocks": clk,
         "cpu_baseline": cpu,
         "exact_fallbacks_per_frame": stats["exact_fallbacks"] / max(stats["frames_inserted"], 1),
+        "other_configs": others,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
-    grid.close()
+    if others is None:
+        grid.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -424,6 +480,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--latency-frames", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip cfg1/cfg3/cfg5 lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

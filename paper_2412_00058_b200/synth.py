@@ -257,3 +257,16 @@ def small_fan(seed=13, nframes=8, lines=24, samples=96, dims=(64, 56, 40), voxel
         t = (0.5 * dims[0] * voxel, 1.0, 5.0 + 0.8 * k)
         return q, t
     return Workload("small_fan", calib, dims, voxel, (0.0, 0.0, 0.0), _poses(nframes, f, seed), 1, seed)
+
+
+def synth_frames_device(wl: Workload, dst, first: int, n: int, device: int = 0, stream=None):
+    """Fill `dst` (device u8 tensor / pointer, n x h x w) with frames [first, first+n) from the
+    device generator svr_synth_frames (same model as synth_frames_np)."""
+    base = dst.data_ptr() if hasattr(dst, "data_ptr") else int(dst)
+    fb = wl.w * wl.h
+    for a in range(0, n, 4096):
+        m = min(4096, n - a)
+        _abi.check(_abi.lib().svr_synth_frames(
+            base + a * fb, wl.w, wl.h, first + a, m, wl.calib,
+            _abi.rigid_ptr(np.ascontiguousarray(wl.poses[first + a:first + a + m])), wl.kind, wl.seed,
+            device, stream))
