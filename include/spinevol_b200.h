@@ -98,6 +98,7 @@ typedef struct svr_stats {
     uint64_t pixels_saturated; /* voxels found above the SPEC caps at readout */
     uint64_t exact_fallbacks;  /* pixels resolved by the exact fp64 chain (near .5 ties) */
     uint64_t kernel_launches;  /* kernels this handle launched (all kinds) */
+    uint64_t chunks_deferred;  /* 16-px chunks sent to the exact per-pixel pass (ties, edges) */
 } svr_stats;
 
 /* Depth-band coronal render (BASELINE cfg4).  Depth axis = grid y, depth(y) = y*voxel_mm.

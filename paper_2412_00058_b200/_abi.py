@@ -64,7 +64,7 @@ class Stats(C.Structure):
     _fields_ = [("frames_inserted", C.c_uint64), ("pixels_inserted", C.c_uint64),
                 ("pixels_oob", C.c_uint64), ("pixels_skipped_zero", C.c_uint64),
                 ("pixels_saturated", C.c_uint64), ("exact_fallbacks", C.c_uint64),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("chunks_deferred", C.c_uint64)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}

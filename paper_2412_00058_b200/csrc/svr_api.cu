@@ -82,7 +82,10 @@ struct svr_volume {
     double fan_angle = 0.0;
     uint64_t launches = 0;
     uint64_t frames = 0;
-    int insert_kernel = 1;      // SVR_INSERT_KERNEL: 1 direct (default), 3 plane, 0 rows, 2 tile
+    ull* d_work = nullptr;          // deferred exact-path chunks of k_pnn_plane
+    unsigned int* d_work_n = nullptr;
+    unsigned int work_cap = 0;
+    int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
 };
 
 // ---------------------------------------------------------------- host geometry (exact)
@@ -224,10 +227,20 @@ static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid
     fp->pose = pose;
     fp->cal = dev_calib(c);
     fp->g = dev_grid(g);
-    // image-plane normal in voxel space = third column of R_pose R_calib (k_pnn_plane table)
+    // image-plane normal in voxel space = third column of R_pose R_calib (k_pnn_plane table);
+    // the plane passes through K (image origin).  z_c(x,y) = K_z - (n_x (x-K_x) + n_y (y-K_y))/n_z
     {
-        const long double nx = std::fabs(a.Mv[2]), ny = std::fabs(a.Mv[5]), nz = std::fabs(a.Mv[8]);
-        fp->plane_ok = (nx + ny) < 0.99L * nz ? 1 : 0;
+        const long double nx = a.Mv[2], ny = a.Mv[5], nz = a.Mv[8];
+        const long double ax = std::fabs(nx), ay = std::fabs(ny), az = std::fabs(nz);
+        fp->plane_ok = (az > 0 && (ax + ay) < 0.99L * az) ? 1 : 0;
+        if (fp->plane_ok) {
+            fp->pz[0] = (double)(a.K[2] + (nx * a.K[0] + ny * a.K[1]) / nz);
+            fp->pz[1] = (double)(-nx / nz);
+            fp->pz[2] = (double)(-ny / nz);
+            fp->pz[3] = (double)((ax + ay) / (2 * az) + 0.5L + 1e-7L);
+        } else {
+            fp->pz[0] = fp->pz[1] = fp->pz[2] = fp->pz[3] = 0.0;
+        }
     }
     return SVR_OK;
 }
@@ -495,6 +508,8 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFree(v->d_boxes);
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
+    cudaFree(v->d_work);
+    cudaFree(v->d_work_n);
     for (int i = 0; i < 2; ++i) {
         cudaFree(v->d_stage[i]);
         cudaFreeHost(v->h_stage[i]);
@@ -522,8 +537,8 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
                            : !std::strcmp(e, "tile")   ? 2
-                           : !std::strcmp(e, "plane")  ? 3
-                                                       : 1;
+                           : !std::strcmp(e, "direct") ? 1
+                                                       : 3;
 
     v->device = device;
     auto bail = [&](int code) {
@@ -729,9 +744,10 @@ struct TileShape {
     int tw, th, ntx, nty;
 };
 
-static bool tile_ok(const svr_volume* v, const DevCalib& cal, int w, int h, TileShape* ts) {
+static bool tile_ok(const svr_volume* v, const DevCalib& cal, int w, int h, TileShape* ts,
+                    int max_tw) {
     const int cpr = (w + kChunk - 1) / kChunk;
-    ts->tw = std::min(8, cpr);
+    ts->tw = std::min(max_tw, cpr);
     while (256 % ts->tw) --ts->tw;
     ts->th = 256 / ts->tw;
     ts->ntx = (cpr + ts->tw - 1) / ts->tw;
@@ -787,8 +803,8 @@ static void launch_rows_t(svr_volume* v, const uint8_t* px, long long pitch, lon
 }
 
 // Launch over frames resident in device memory, chunked to the grid.y limit.
-//   PNN insert: k_insert direct (default), k_pnn_plane (SVR_INSERT_KERNEL=plane, when tile_ok
-//   and no skip_zero), k_pnn_rows (=rows),
+//   PNN insert: k_pnn_plane + k_pnn_work (default, when tile_ok and no skip_zero), k_insert
+//   direct (SVR_INSERT_KERNEL=direct, skip_zero, narrow tiles), k_pnn_rows (=rows),
 //   k_pnn_tile (SVR_INSERT_KERNEL=tile, when tile_ok); footprint / trilinear: k_insert.
 static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long pitch,
                          long long fstride, int w, int h, int n, const FrameParams* fps,
@@ -797,10 +813,9 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     const bool vec = ((uintptr_t)px % 16 == 0) && (pitch % 16 == 0) && (fstride % 16 == 0) &&
                      (w % kChunk == 0);
     TileShape ts;
-    const bool tiled = mode == kModeInsert && (v->insert_kernel == 2 || v->insert_kernel == 3) &&
-                       tile_ok(v, cal, w, h, &ts);
-    const bool tile = tiled && v->insert_kernel == 2;
-    const bool plane = tiled && v->insert_kernel == 3 && !skip;
+    const bool tile = mode == kModeInsert && v->insert_kernel == 2 && tile_ok(v, cal, w, h, &ts, 8);
+    const bool plane = mode == kModeInsert && v->insert_kernel == 3 && !skip &&
+                       tile_ok(v, cal, w, h, &ts, 4);
     const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
@@ -808,15 +823,28 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
         int* bx = boxes ? boxes + 6 * k0 : nullptr;
         if (plane) {
             const int cpr = (w + kChunk - 1) / kChunk;
-            dim3 grid(ts.ntx * ts.nty, m);
-            if (vec) {
-                if (box) k_pnn_plane<true, true><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
-                else k_pnn_plane<true, false><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
-            } else {
-                if (box) k_pnn_plane<false, true><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
-                else k_pnn_plane<false, false><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, fps + k0, cal, v->d_fan, dev_grid(v->d), v->acc, bx, stats);
+            if (!v->d_work) {
+                v->work_cap = 1u << 20;
+                CK(cudaMalloc(&v->d_work, sizeof(ull) * v->work_cap));
+                CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
             }
-            v->launches++;
+            CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
+            dim3 grid(ts.ntx * ts.nty, m);
+            const GridDev gd = dev_grid(v->d);
+#define LP(a, b)                                                                                  \
+    k_pnn_plane<a, b><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, \
+                                                   fps + k0, cal, v->d_fan, gd, v->acc, bx, stats,  \
+                                                   v->d_work, v->d_work_n, v->work_cap);           \
+    k_pnn_work<a, b><<<148 * 8, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,  \
+                                                     gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
+                                                     v->work_cap)
+            if (vec) {
+                if (box) { LP(true, true); } else { LP(true, false); }
+            } else {
+                if (box) { LP(false, true); } else { LP(false, false); }
+            }
+#undef LP
+            v->launches += 2;
         } else if (rows) {
             if (vec) {
                 if (box) launch_rows_t<true, true>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
@@ -1256,6 +1284,7 @@ extern "C" int svr_get_stats(svr_volume* v, svr_stats* out) {
     out->pixels_saturated = h[kStSaturated];
     out->exact_fallbacks = h[kStFallback];
     out->kernel_launches = v->launches;
+    out->chunks_deferred = h[kStDeferred];
     return SVR_OK;
 }
 
