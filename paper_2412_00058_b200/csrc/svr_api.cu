@@ -232,12 +232,12 @@ static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid
     {
         const long double nx = a.Mv[2], ny = a.Mv[5], nz = a.Mv[8];
         const long double ax = std::fabs(nx), ay = std::fabs(ny), az = std::fabs(nz);
-        fp->plane_ok = (az > 0 && (ax + ay) < 0.99L * az) ? 1 : 0;
+        fp->plane_ok = (az > 0 && (ax + ay) < 0.99L * az) ? 1 : 0;  // 2h = s + 1.004 < 2
         if (fp->plane_ok) {
             fp->pz[0] = (double)(a.K[2] + (nx * a.K[0] + ny * a.K[1]) / nz);
             fp->pz[1] = (double)(-nx / nz);
             fp->pz[2] = (double)(-ny / nz);
-            fp->pz[3] = (double)((ax + ay) / (2 * az) + 0.5L + 1e-7L);
+            fp->pz[3] = (double)((ax + ay) / (2 * az) + 0.5L + 2e-3L);
         } else {
             fp->pz[0] = fp->pz[1] = fp->pz[2] = fp->pz[3] = 0.0;
         }
