@@ -814,7 +814,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                      (w % kChunk == 0);
     TileShape ts;
     const bool tile = mode == kModeInsert && v->insert_kernel == 2 && tile_ok(v, cal, w, h, &ts, 8);
-    const bool plane = mode == kModeInsert && v->insert_kernel == 3 && !skip &&
+    const bool plane = mode == kModeInsert && v->insert_kernel == 3 && !skip && w >= 4 * kChunk &&
                        tile_ok(v, cal, w, h, &ts, 4);
     const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
     for (int k0 = 0; k0 < n; k0 += 65535) {
@@ -829,12 +829,13 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                 CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
             }
             CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
-            dim3 grid(ts.ntx * ts.nty, m);
+            const int ntx = (cpr + kPlaneTW - 1) / kPlaneTW, nty = (h + kPlaneTH - 1) / kPlaneTH;
+            dim3 grid(ntx, m, nty);
             const GridDev gd = dev_grid(v->d);
 #define LP(a, b)                                                                                  \
-    k_pnn_plane<a, b><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, \
-                                                   fps + k0, cal, v->d_fan, gd, v->acc, bx, stats,  \
-                                                   v->d_work, v->d_work_n, v->work_cap);           \
+    k_pnn_plane<a, b><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,      \
+                                                   v->d_fan, gd, v->acc, bx, stats, v->d_work,     \
+                                                   v->d_work_n, v->work_cap);                      \
     k_pnn_work<a, b><<<148 * 8, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,  \
                                                      gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
                                                      v->work_cap)
