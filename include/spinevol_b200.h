@@ -162,11 +162,20 @@ int svr_insert_frames(svr_volume* vol, const uint8_t* px, int64_t row_pitch, int
 int svr_fill_holes(svr_volume* vol, const svr_box* region, int32_t mode, int32_t radius,
                    int64_t* filled_out);
 
+/* fill_holes over a list of regions in one launch (e.g. the union of a batch's dirty boxes,
+ * one per z-chunk).  Regions should not overlap: an overlap is recomputed identically but
+ * counted twice in filled_out. */
+int svr_fill_holes_boxes(svr_volume* vol, const svr_box* regions, int32_t n, int32_t mode,
+                         int32_t radius, int64_t* filled_out);
+
 /* Depth-band coronal render (BASELINE cfg4), incremental: recompute the columns a change
  * inside `dirty` can affect (dirty (+) fill_radius for depths, (+) median_radius for the
  * image).  dirty = NULL re-renders every column of the slab. */
 int svr_render_coronal(svr_volume* vol, const svr_box* dirty, int32_t fill_radius,
                        const svr_render_params* params);
+/* svr_render_coronal for a list of dirty regions in one pair of launches. */
+int svr_render_coronal_boxes(svr_volume* vol, const svr_box* dirty, int32_t n, int32_t fill_radius,
+                             const svr_render_params* params);
 /* Copy rendered rows z in [z0,z1] (global, inside the slab) as nx-wide row-major images. */
 int svr_read_coronal(svr_volume* vol, int32_t z0, int32_t z1, float* mean_out, float* max_out,
                      int32_t* depth_out);

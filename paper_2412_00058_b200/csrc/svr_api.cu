@@ -83,9 +83,13 @@ struct svr_volume {
     uint64_t launches = 0;
     uint64_t frames = 0;
     ull* d_work = nullptr;          // deferred exact-path chunks of k_pnn_plane
+    void* d_tiles = nullptr;        // region tables of the multi-box fill / render launches
+    size_t tiles_cap = 0;
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
+    bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
+    int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
 };
 
 // ---------------------------------------------------------------- host geometry (exact)
@@ -227,6 +231,16 @@ static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid
     fp->pose = pose;
     fp->cal = dev_calib(c);
     fp->g = dev_grid(g);
+    // Tie window: |fixed - real| <= 2^-33 (1 + row + col) (coefficient rounding, exact integer
+    // steps) + 1e-9 (fp64 chain vs real arithmetic).  Use the smallest power of two
+    // >= 4x that bound, in 2^-32 voxel units (2^-21 for cfg2, at most 2^-16).
+    {
+        const double bound = std::ldexp(1.0, -33) * (double)(c.crop_w + c.crop_h + 1) + 1e-9;
+        const double target = 4.0 * bound * 4294967296.0;
+        int e = 4;
+        while (e < 16 && std::ldexp(1.0, e) < target) ++e;
+        fp->tie_eps = 1u << e;
+    }
     // image-plane normal in voxel space = third column of R_pose R_calib (k_pnn_plane table);
     // the plane passes through K (image origin).  z_c(x,y) = K_z - (n_x (x-K_x) + n_y (y-K_y))/n_z
     {
@@ -509,6 +523,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
     cudaFree(v->d_work);
+    cudaFree(v->d_tiles);
     cudaFree(v->d_work_n);
     for (int i = 0; i < 2; ++i) {
         cudaFree(v->d_stage[i]);
@@ -534,6 +549,8 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     if (device < 0 || device >= ndev) return fail(SVR_E_INVALID, "device %d out of range", device);
     svr_volume* v = new svr_volume();
     v->d = *desc;
+    if (const char* e = std::getenv("SVR_FILL_KERNEL")) v->fill_smem = !std::strcmp(e, "smem");
+    if (const char* e = std::getenv("SVR_FILL_ZC")) v->fill_zc = std::atoi(e);
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
                            : !std::strcmp(e, "tile")   ? 2
@@ -836,7 +853,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     k_pnn_plane<a, b><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,      \
                                                    v->d_fan, gd, v->acc, bx, stats, v->d_work,     \
                                                    v->d_work_n, v->work_cap);                      \
-    k_pnn_work<a, b><<<148 * 8, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,  \
+    k_pnn_work<a, b><<<4096, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,     \
                                                      gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
                                                      v->work_cap)
             if (vec) {
@@ -1034,19 +1051,56 @@ static bool clip_box(const svr_volume* v, const svr_box* in, Box* out) {
     return b.x0 <= b.x1 && b.y0 <= b.y1 && b.z0 <= b.z1;
 }
 
-extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode, int32_t radius,
-                              int64_t* filled_out) {
-    VOL_CHECK(v);
-    if (!v->acc) return fail(SVR_E_INVALID, "fill_holes needs a PNN volume");
-    if (mode != SVR_FILL_MEAN && mode != SVR_FILL_MEDIAN) return fail(SVR_E_INVALID, "unknown fill mode");
-    if (radius < 1 || radius > 8) return fail(SVR_E_INVALID, "fill radius must be in [1,8]");
-    if (mode == SVR_FILL_MEAN && (2 * radius + 1) * (2 * radius + 1) * (2 * radius + 1) * 255 > 65535)
-        return fail(SVR_E_INVALID, "mean fill radius too large for the 16-bit fill payload");
-    Box b;
-    const bool any = clip_box(v, region, &b);
-    if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
-    if (any) {
-        const GridDev g = dev_grid(v->d);
+// Upload a small region table to the handle's device scratch (stream-ordered: the copy runs after
+// every earlier kernel of the stream, so one buffer serves consecutive launches).
+static int upload_tiles(svr_volume* v, const void* host, size_t bytes, void** dev) {
+    if (bytes > v->tiles_cap) {
+        CK(cudaStreamSynchronize(v->stream));
+        cudaFree(v->d_tiles);
+        v->d_tiles = nullptr;
+        v->tiles_cap = 0;
+        CK(cudaMalloc(&v->d_tiles, std::max<size_t>(bytes, 4096)));
+        v->tiles_cap = std::max<size_t>(bytes, 4096);
+    }
+    CK(cudaMemcpyAsync(v->d_tiles, host, bytes, cudaMemcpyHostToDevice, v->stream));
+    *dev = v->d_tiles;
+    return SVR_OK;
+}
+
+static dim3 grid_1d(long long n) {
+    const long long gx = std::min<long long>(n, 65535);
+    return dim3((unsigned)gx, (unsigned)((n + gx - 1) / gx));
+}
+
+// Launch the fill over a list of clipped, non-empty boxes.
+static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, int32_t radius) {
+    const GridDev g = dev_grid(v->d);
+    if (mode == SVR_FILL_MEAN && radius == 1 && !v->fill_smem) {
+        const int zc = v->fill_zc;
+        std::vector<BoxTiles> bt;
+        long long total = 0;
+        for (const Box& b : bs) {
+            BoxTiles t;
+            t.b = b;
+            t.ntx = (b.x1 - b.x0 + 1 + 119) / 120;
+            t.nty = (b.y1 - b.y0 + 1 + 7) / 8;
+            t.first = total;
+            total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
+            bt.push_back(t);
+        }
+        void* d = nullptr;
+        if (int e = upload_tiles(v, bt.data(), sizeof(BoxTiles) * bt.size(), &d)) return e;
+        const dim3 grd = grid_1d(total);
+        const BoxTiles* dt = (const BoxTiles*)d;
+        const int nb = (int)bt.size();
+        if (zc == 8) k_fill_warp<8><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter);
+        else if (zc == 32) k_fill_warp<32><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter);
+        else k_fill_warp<16><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter);
+        v->launches++;
+        CKL();
+        return SVR_OK;
+    }
+    for (const Box& b : bs) {
         const int bx = b.x1 - b.x0 + 1, by = b.y1 - b.y0 + 1, bz = b.z1 - b.z0 + 1;
         if (mode == SVR_FILL_MEAN && radius <= 2) {
             dim3 grd((bx + 31) / 32, (by + 7) / 8, (bz + 31) / 32);
@@ -1067,6 +1121,19 @@ extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode
         v->launches++;
         CKL();
     }
+    return SVR_OK;
+}
+
+static int check_fill_args(svr_volume* v, int32_t mode, int32_t radius) {
+    if (!v->acc) return fail(SVR_E_INVALID, "fill_holes needs a PNN volume");
+    if (mode != SVR_FILL_MEAN && mode != SVR_FILL_MEDIAN) return fail(SVR_E_INVALID, "unknown fill mode");
+    if (radius < 1 || radius > 8) return fail(SVR_E_INVALID, "fill radius must be in [1,8]");
+    if (mode == SVR_FILL_MEAN && (2 * radius + 1) * (2 * radius + 1) * (2 * radius + 1) * 255 > 65535)
+        return fail(SVR_E_INVALID, "mean fill radius too large for the 16-bit fill payload");
+    return SVR_OK;
+}
+
+static int finish_count(svr_volume* v, int64_t* filled_out) {
     if (filled_out) {
         ull c = 0;
         CK(cudaMemcpyAsync(&c, v->d_counter, sizeof(ull), cudaMemcpyDeviceToHost, v->stream));
@@ -1074,6 +1141,34 @@ extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode
         *filled_out = (int64_t)c;
     }
     return SVR_OK;
+}
+
+extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode, int32_t radius,
+                              int64_t* filled_out) {
+    VOL_CHECK(v);
+    if (int e = check_fill_args(v, mode, radius)) return e;
+    Box b;
+    const bool any = clip_box(v, region, &b);
+    if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
+    if (any)
+        if (int e = fill_boxes(v, std::vector<Box>{b}, mode, radius)) return e;
+    return finish_count(v, filled_out);
+}
+
+extern "C" int svr_fill_holes_boxes(svr_volume* v, const svr_box* regions, int32_t n, int32_t mode,
+                                    int32_t radius, int64_t* filled_out) {
+    VOL_CHECK(v);
+    if (int e = check_fill_args(v, mode, radius)) return e;
+    if (n < 0 || (n > 0 && !regions)) return fail(SVR_E_INVALID, "bad region list");
+    std::vector<Box> bs;
+    for (int i = 0; i < n; ++i) {
+        Box b;
+        if (clip_box(v, &regions[i], &b)) bs.push_back(b);
+    }
+    if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
+    if (!bs.empty())
+        if (int e = fill_boxes(v, bs, mode, radius)) return e;
+    return finish_count(v, filled_out);
 }
 
 // Integer render parameters — identical formula to oracle orc_render_ints.
@@ -1089,9 +1184,41 @@ static void render_ints(const svr_render_params* p, double vx, int ny, int* ylo,
     *below = (int)std::lround(p->band_below_mm / vx);
 }
 
-extern "C" int svr_render_coronal(svr_volume* v, const svr_box* dirty, int32_t fill_radius,
-                                  const svr_render_params* p) {
-    VOL_CHECK(v);
+// Depth/band column regions of one dirty box (or the whole slab for dirty == NULL), clipped.
+static bool render_regions(const svr_volume* v, const svr_box* dirty, int fr, int R, ColTiles* d,
+                           ColTiles* m) {
+    const int zb = v->d.z_begin, ze = v->d.z_end - 1, nxm = v->d.nx - 1;
+    int dx0 = 0, dx1 = nxm, dz0 = zb, dz1 = ze;
+    if (dirty) {
+        if (dirty->x0 > dirty->x1) return false;
+        if (dirty->x1 + fr + R < 0 || dirty->x0 - fr - R > nxm || dirty->z1 + fr + R < zb ||
+            dirty->z0 - fr - R > ze)
+            return false;
+        dx0 = dirty->x0 - fr;
+        dx1 = dirty->x1 + fr;
+        dz0 = dirty->z0 - fr;
+        dz1 = dirty->z1 + fr;
+    }
+    int mx0 = dx0 - R, mx1 = dx1 + R, mz0 = dz0 - R, mz1 = dz1 + R;
+    auto cx = [&](int a) { return std::min(std::max(a, 0), nxm); };
+    auto cz = [&](int a) { return std::min(std::max(a, zb), ze); };
+    *d = ColTiles{cx(dx0), cx(dx1), cz(dz0), cz(dz1), 0, 0};
+    *m = ColTiles{cx(mx0), cx(mx1), cz(mz0), cz(mz1), 0, 0};
+    return true;
+}
+
+static long long tile_cols(std::vector<ColTiles>& ct) {
+    long long total = 0;
+    for (ColTiles& t : ct) {
+        t.ntx = (t.x1 - t.x0 + 1 + 127) / 128;
+        t.first = total;
+        total += (long long)t.ntx * (t.z1 - t.z0 + 1);
+    }
+    return total;
+}
+
+static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill_radius,
+                        const svr_render_params* p) {
     if (!v->acc) return fail(SVR_E_INVALID, "render needs a PNN volume");
     if (!p) return fail(SVR_E_INVALID, "render params NULL");
     if (p->median_radius < 0 || p->median_radius > 2)
@@ -1099,42 +1226,47 @@ extern "C" int svr_render_coronal(svr_volume* v, const svr_box* dirty, int32_t f
     if (fill_radius < 0) return fail(SVR_E_INVALID, "negative fill radius");
     int ylo, yhi, above, below;
     render_ints(p, v->d.voxel_mm, v->d.ny, &ylo, &yhi, &above, &below);
-    const int R = p->median_radius;
-    const int zb = v->d.z_begin, ze = v->d.z_end - 1, nxm = v->d.nx - 1;
-    int dx0 = 0, dx1 = nxm, dz0 = zb, dz1 = ze;
-    if (dirty) {
-        if (dirty->x0 > dirty->x1) return SVR_OK;
-        dx0 = dirty->x0 - fill_radius;
-        dx1 = dirty->x1 + fill_radius;
-        dz0 = dirty->z0 - fill_radius;
-        dz1 = dirty->z1 + fill_radius;
+    std::vector<ColTiles> dt, mt;
+    for (int i = 0; i < std::max(n, 1); ++i) {
+        ColTiles d, m;
+        if (render_regions(v, dirty ? &dirty[i] : nullptr, fill_radius, p->median_radius, &d, &m)) {
+            dt.push_back(d);
+            mt.push_back(m);
+        }
     }
-    int mx0 = dx0 - R, mx1 = dx1 + R, mz0 = dz0 - R, mz1 = dz1 + R;
-    auto cx = [&](int a) { return std::min(std::max(a, 0), nxm); };
-    auto cz = [&](int a) { return std::min(std::max(a, zb), ze); };
-    dx0 = cx(dx0); dx1 = cx(dx1); mx0 = cx(mx0); mx1 = cx(mx1);
-    dz0 = cz(dz0); dz1 = cz(dz1); mz0 = cz(mz0); mz1 = cz(mz1);
-    if (dirty && (dirty->x1 < 0 || dirty->x0 > nxm || dirty->z1 + fill_radius + R < zb ||
-                  dirty->z0 - fill_radius - R > ze))
-        return SVR_OK;
+    if (dt.empty()) return SVR_OK;
+    const long long nd = tile_cols(dt), nm = tile_cols(mt);
+    // one upload holds both tables: [dt | mt]
+    std::vector<ColTiles> both(dt);
+    both.insert(both.end(), mt.begin(), mt.end());
+    void* d = nullptr;
+    if (int e = upload_tiles(v, both.data(), sizeof(ColTiles) * both.size(), &d)) return e;
+    const ColTiles* ddt = (const ColTiles*)d;
+    const ColTiles* dmt = ddt + dt.size();
     const GridDev g = dev_grid(v->d);
-    for (int z0 = dz0; z0 <= dz1; z0 += 65535) {
-        int nzs = std::min(65535, dz1 - z0 + 1);
-        dim3 grd((dx1 - dx0 + 1 + 127) / 128, nzs);
-        k_depth<<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dx0, dx1, z0, ylo, yhi, p->fill_mode,
-                                            v->r_depth);
-        v->launches++;
-        CKL();
-    }
-    for (int z0 = mz0; z0 <= mz1; z0 += 65535) {
-        int nzs = std::min(65535, mz1 - z0 + 1);
-        dim3 grd((mx1 - mx0 + 1 + 127) / 128, nzs);
-        k_band<<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, mx0, mx1, z0, R, above, below,
-                                           p->fill_mode, v->r_depth, v->r_mdepth, v->r_mean, v->r_max);
-        v->launches++;
-        CKL();
-    }
+    k_depth<<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
+                                                 p->fill_mode, v->r_depth);
+    v->launches++;
+    CKL();
+    k_band<<<grid_1d(nm), 128, 0, v->stream>>>(v->acc, v->fill, g, dmt, (int)mt.size(), p->median_radius,
+                                                above, below, p->fill_mode, v->r_depth, v->r_mdepth,
+                                                v->r_mean, v->r_max);
+    v->launches++;
+    CKL();
     return SVR_OK;
+}
+
+extern "C" int svr_render_coronal(svr_volume* v, const svr_box* dirty, int32_t fill_radius,
+                                  const svr_render_params* p) {
+    VOL_CHECK(v);
+    return render_boxes(v, dirty, dirty ? 1 : 0, fill_radius, p);
+}
+
+extern "C" int svr_render_coronal_boxes(svr_volume* v, const svr_box* dirty, int32_t n,
+                                        int32_t fill_radius, const svr_render_params* p) {
+    VOL_CHECK(v);
+    if (n <= 0 || !dirty) return n == 0 ? SVR_OK : fail(SVR_E_INVALID, "bad region list");
+    return render_boxes(v, dirty, n, fill_radius, p);
 }
 
 extern "C" int svr_read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv,

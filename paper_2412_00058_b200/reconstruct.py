@@ -145,7 +145,22 @@ class VoxelGrid:
                                    mode, radius, C.byref(out) if count else None))
         return int(out.value) if count else None
 
+    def fill_holes_boxes(self, regions, radius: int = 1, mode: int = _abi.FILL_MEAN,
+                         count: bool = True) -> Optional[int]:
+        """fill_holes over a list of (non-overlapping) regions in one launch."""
+        arr = (Box * max(len(regions), 1))(*[_box(r) for r in regions])
+        out = C.c_int64(0)
+        check(lib().svr_fill_holes_boxes(self._h, arr, len(regions), mode, radius,
+                                         C.byref(out) if count else None))
+        return int(out.value) if count else None
+
     # -- project
+    def render_coronal_boxes(self, dirty, params: RenderParams = None, fill_radius: int = 1):
+        from .synth import render_params
+        params = params or render_params()
+        arr = (Box * max(len(dirty), 1))(*[_box(r) for r in dirty])
+        check(lib().svr_render_coronal_boxes(self._h, arr, len(dirty), fill_radius, C.byref(params)))
+
     def render_coronal(self, dirty=None, params: RenderParams = None, fill_radius: int = 1):
         from .synth import render_params
         params = params or render_params()

@@ -80,3 +80,24 @@ def gather_rows(local, slab: Slab, slabs, dist):
         buf = torch.cat(lst, 0)
     parts = [buf[r * rows_max: r * rows_max + (slabs[r].owned[1] - slabs[r].owned[0])] for r in range(world)]
     return torch.cat(parts, 0)
+
+
+def chunk_boxes(boxes, idx, alloc, chunk: int = 32, dilate: int = 0):
+    """Dirty region of a batch as non-overlapping per-z-chunk boxes: for every chunk of `chunk`
+    planes of the stored slab, the bounding box of the routed frames' boxes (each dilated by
+    `dilate`) that meet it, clipped to the chunk.  Much tighter than one bounding box for a
+    sweep that drifts laterally; fill/render over it give the same result (every non-empty
+    voxel and every voxel within `dilate` of one lies inside)."""
+    out = []
+    if len(idx) == 0:
+        return out
+    bs = [boxes[int(k)] for k in idx if not boxes[int(k)].empty()]
+    d = dilate
+    for z0 in range(alloc[0], alloc[1], chunk):
+        z1 = min(z0 + chunk, alloc[1]) - 1
+        sel = [b for b in bs if b.z1 + d >= z0 and b.z0 - d <= z1]
+        if not sel:
+            continue
+        out.append(_abi.Box(min(b.x0 for b in sel) - d, min(b.y0 for b in sel) - d, z0,
+                            max(b.x1 for b in sel) + d, max(b.y1 for b in sel) + d, z1))
+    return out

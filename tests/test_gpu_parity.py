@@ -268,3 +268,49 @@ def test_cfg1_all_kernels(kernel, monkeypatch):
     rboxes = ref.insert_frames(frames, wl.poses, wl.calib)
     _assert_acc(grid, ref)
     assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
+
+
+@pytest.mark.parametrize("fill_kernel", ["warp", "smem"])
+def test_mean_fill_kernels_bitexact(fill_kernel, monkeypatch):
+    """Both r=1 mean-fill kernels (register/shuffle and shared-memory separable) against the
+    oracle on a region with grid-edge clipping."""
+    monkeypatch.setenv("SVR_FILL_KERNEL", fill_kernel)
+    wl = synth.cfg1(nframes=80)
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    grid.insert_frames(frames, wl.poses, wl.calib)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_frames(frames, wl.poses, wl.calib)
+    for region in (None, (3, 0, 20, 200, 127, 70), (0, 5, 0, 127, 60, 255)):
+        n = grid.fill_holes(region, 1, pkg.FILL_MEAN)
+        nr = ref.fill_holes(region, 0, 1)
+        assert n == nr, region
+        assert np.array_equal(grid.fill_layer(), ref.fill), region
+
+
+def test_chunked_dirty_regions_equal_bounding_box():
+    """Batch fill/render over per-z-chunk dirty boxes (svr_fill_holes_boxes,
+    svr_render_coronal_boxes) equals the same over one bounding box, bit for bit."""
+    from paper_2412_00058_b200 import sharding
+    wl = synth.cfg2(nframes=240)
+    idx = np.arange(0, 240, 1)
+    frames = np.stack([wl.frames_np(int(k), 1)[0] for k in idx[:120]])
+    poses = wl.poses[:120]
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, poses)
+    alloc = (0, wl.dims[2])
+    u = sharding.union_box(boxes, np.arange(len(boxes)), alloc)
+    rp = synth.render_params()
+    a = _grid(wl)
+    a.insert_frames(frames, poses, wl.calib)
+    na = a.fill_holes(pkg.dilate(u, 1), 1, pkg.FILL_MEAN)
+    a.render_coronal(u, rp, 1)
+    b = _grid(wl)
+    b.insert_frames(frames, poses, wl.calib)
+    fb = sharding.chunk_boxes(boxes, np.arange(len(boxes)), alloc, chunk=32, dilate=1)
+    nb = b.fill_holes_boxes(fb, 1, pkg.FILL_MEAN)
+    b.render_coronal_boxes(sharding.chunk_boxes(boxes, np.arange(len(boxes)), alloc, chunk=32), rp, 1)
+    box = (u.x0 - 1, max(u.y0 - 1, 0), max(u.z0 - 1, 0), u.x1 + 1, min(u.y1 + 1, wl.dims[1] - 1), u.z1 + 1)
+    assert np.array_equal(a.fill_layer(box), b.fill_layer(box))
+    assert na == nb
+    for x, y in zip(a.read_coronal(), b.read_coronal()):
+        assert np.array_equal(x, y)
