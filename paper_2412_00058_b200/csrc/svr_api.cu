@@ -62,10 +62,13 @@ struct svr_volume {
     ull* d_stats = nullptr;  // kStCount counters
     ull* d_counter = nullptr;
     // per-frame parameter staging
-    FrameParams* h_params = nullptr;
+    // double-buffered host side: the next call fills one pinned buffer while the previous
+    // call's upload from the other is still queued behind that call's kernels
+    FrameParams* h_params[2] = {nullptr, nullptr};
     FrameParams* d_params = nullptr;
     int params_cap = 0;
-    cudaEvent_t params_ev = nullptr;
+    int pslot = 0;
+    cudaEvent_t params_ev[2] = {nullptr, nullptr};
     int* d_boxes = nullptr;
     int* h_boxes = nullptr;
     int boxes_cap = 0;
@@ -94,10 +97,10 @@ struct svr_volume {
 
 // ---------------------------------------------------------------- host geometry (exact)
 // Rotation of Quat::rotate (geometry.hpp:44-49) as the linear map it computes in real
-// arithmetic, M = I + 2w[u]x + 2(u u^T - |u|^2 I), evaluated in long double.
-static void quat_mat(const svr_rigid& q, long double M[9]) {
-    const long double w = q.qw, x = q.qx, y = q.qy, z = q.qz;
-    const long double n2 = x * x + y * y + z * z;
+// arithmetic, M = I + 2w[u]x + 2(u u^T - |u|^2 I), evaluated in double.
+static void quat_mat(const svr_rigid& q, double M[9]) {
+    const double w = q.qw, x = q.qx, y = q.qy, z = q.qz;
+    const double n2 = x * x + y * y + z * z;
     M[0] = 1 + 2 * (x * x - n2);
     M[1] = 2 * (x * y) - 2 * w * z;
     M[2] = 2 * (x * z) + 2 * w * y;
@@ -109,34 +112,16 @@ static void quat_mat(const svr_rigid& q, long double M[9]) {
     M[8] = 1 + 2 * (z * z - n2);
 }
 
-static void mat_mul(const long double A[9], const long double B[9], long double C[9]) {
+static void mat_mul(const double A[9], const double B[9], double C[9]) {
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
             C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
 }
 
 struct Affine {  // u = K + Mv * p, voxel units (no +1/2)
-    long double Mv[9];
-    long double K[3];
+    double Mv[9];
+    double K[3];
 };
-
-static Affine frame_affine(const svr_rigid& pose, const svr_calib& c, const svr_grid_desc& g) {
-    long double Mp[9], Mc[9], Mv[9];
-    quat_mat(pose, Mp);
-    quat_mat(c.image_to_transducer, Mc);
-    mat_mul(Mp, Mc, Mv);
-    Affine a;
-    const long double v = g.voxel_mm;
-    const long double tc[3] = {c.image_to_transducer.tx, c.image_to_transducer.ty,
-                               c.image_to_transducer.tz};
-    const long double tp[3] = {pose.tx, pose.ty, pose.tz};
-    for (int k = 0; k < 3; ++k) {
-        long double r = Mp[3 * k] * tc[0] + Mp[3 * k + 1] * tc[1] + Mp[3 * k + 2] * tc[2];
-        a.K[k] = (r + tp[k] - (long double)g.origin_mm[k]) / v;
-        for (int j = 0; j < 3; ++j) a.Mv[3 * k + j] = Mv[3 * k + j] / v;
-    }
-    return a;
-}
 
 // Fan scanline directions (pin identical to oracle/svr_oracle.c orc_fan_table).
 static void fan_table(const svr_calib& c, std::vector<double>& s, std::vector<double>& co) {
@@ -180,13 +165,13 @@ static int check_calib(const svr_calib* c, int32_t w, int32_t h) {
     return SVR_OK;
 }
 
-static long long to_fixed(long double x, bool* ok) {
-    long double s = x * 4294967296.0L;
-    if (!(std::fabs(s) < 4.0e18L)) {
+static long long to_fixed(double x, bool* ok) {
+    double s = x * 4294967296.0;
+    if (!(std::fabs(s) < 4.0e18)) {
         *ok = false;
         return 0;
     }
-    return std::llroundl(s);
+    return std::llround(s);
 }
 
 static DevCalib dev_calib(const svr_calib& c) {
@@ -214,44 +199,104 @@ static GridDev dev_grid(const svr_grid_desc& d) {
     return g;
 }
 
-static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid_desc& g,
+// Pose-independent part of the per-frame map, computed once per insert call.
+struct PrepCtx {
+    double Mc[9];      // image_to_transducer rotation
+    double tc[3];      // image_to_transducer translation (mm)
+    double v;          // voxel_mm
+    double o[3];       // grid origin (mm)
+    double qc2;        // max(1, |q_calib|^2)
+    double base_mm;    // pixel extent from the image origin + |t_calib| + |origin| (mm)
+    double coef_bound; // coefficient rounding part of the tie bound, voxels
+    DevCalib cal;
+    GridDev g;
+};
+
+static double norm3(double a, double b, double c) { return std::sqrt(a * a + b * b + c * c); }
+
+static PrepCtx prep_ctx(const svr_calib& c, const svr_grid_desc& g) {
+    PrepCtx x;
+    quat_mat(c.image_to_transducer, x.Mc);
+    x.tc[0] = c.image_to_transducer.tx;
+    x.tc[1] = c.image_to_transducer.ty;
+    x.tc[2] = c.image_to_transducer.tz;
+    x.v = g.voxel_mm;
+    for (int k = 0; k < 3; ++k) x.o[k] = g.origin_mm[k];
+    const svr_rigid& q = c.image_to_transducer;
+    x.qc2 = std::max(1.0, q.qw * q.qw + q.qx * q.qx + q.qy * q.qy + q.qz * q.qz);
+    const double ext = c.probe == SVR_PROBE_FAN
+                           ? c.fan_r1_mm
+                           : std::hypot((double)c.crop_w * c.scale_x_mm, (double)c.crop_h * c.scale_y_mm);
+    x.base_mm = ext + norm3(x.tc[0], x.tc[1], x.tc[2]) + norm3(x.o[0], x.o[1], x.o[2]);
+    // 32.32 rounding of K + 1/2, Dc, Dr (2^-33 each) plus the host's own fp64 error in Dc, Dr
+    // (|coefficient| <= |M| * scale / v, a few ulps), accumulated over 1 + col + row steps
+    x.coef_bound = (std::ldexp(1.0, -33) + std::ldexp(1.0, -40)) * (double)(c.crop_w + c.crop_h + 1);
+    x.cal = dev_calib(c);
+    x.g = dev_grid(g);
+    return x;
+}
+
+static Affine frame_affine(const svr_rigid& pose, const PrepCtx& x) {
+    double Mp[9], Mv[9];
+    quat_mat(pose, Mp);
+    mat_mul(Mp, x.Mc, Mv);
+    Affine a;
+    const double tp[3] = {pose.tx, pose.ty, pose.tz};
+    for (int k = 0; k < 3; ++k) {
+        double r = Mp[3 * k] * x.tc[0] + Mp[3 * k + 1] * x.tc[1] + Mp[3 * k + 2] * x.tc[2];
+        a.K[k] = (r + tp[k] - x.o[k]) / x.v;
+        for (int j = 0; j < 3; ++j) a.Mv[3 * k + j] = Mv[3 * k + j] / x.v;
+    }
+    return a;
+}
+
+static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, double sy,
                        FrameParams* fp) {
     if (!finite_rigid(pose)) return fail(SVR_E_INVALID, "pose not finite");
-    Affine a = frame_affine(pose, c, g);
+    Affine a = frame_affine(pose, x);
     bool ok = true;
     for (int k = 0; k < 3; ++k) {
-        if (!(std::fabs(a.K[k]) < 1.0e8L)) ok = false;
-        fp->A[k] = to_fixed(a.K[k] + 0.5L, &ok);
-        fp->Dc[k] = to_fixed(a.Mv[3 * k] * (long double)c.scale_x_mm, &ok);
-        fp->Dr[k] = to_fixed(a.Mv[3 * k + 1] * (long double)c.scale_y_mm, &ok);
-        fp->K[k] = (double)a.K[k];
-        for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = (double)a.Mv[3 * k + j];
+        if (!(std::fabs(a.K[k]) < 1.0e8)) ok = false;
+        fp->A[k] = to_fixed(a.K[k] + 0.5, &ok);
+        fp->Dc[k] = to_fixed(a.Mv[3 * k] * sx, &ok);
+        fp->Dr[k] = to_fixed(a.Mv[3 * k + 1] * sy, &ok);
+        fp->K[k] = a.K[k];
+        for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = a.Mv[3 * k + j];
     }
     if (!ok) return fail(SVR_E_INVALID, "pose maps the frame too far from the grid (|u| >= 1e8 voxels)");
     fp->pose = pose;
-    fp->cal = dev_calib(c);
-    fp->g = dev_grid(g);
-    // Tie window: |fixed - real| <= 2^-33 (1 + row + col) (coefficient rounding, exact integer
-    // steps) + 1e-9 (fp64 chain vs real arithmetic).  Use the smallest power of two
-    // >= 4x that bound, in 2^-32 voxel units (2^-21 for cfg2, at most 2^-16).
+    fp->cal = x.cal;
+    fp->g = x.g;
+    // Tie window: |fixed - real| <= coefficient rounding over 1 + col + row exact
+    // integer steps, plus the deviation of an fp64 evaluation from real arithmetic -- the
+    // reference chain's and this host map's (K) alike -- bounded by 512 roundings of the largest
+    // intermediate magnitude qn * R, R = |t_pose| + pixel extent + |t_calib| + |origin| (mm), qn
+    // covering non-unit quaternions.  The window is the smallest power of two >= 4x that bound,
+    // in 2^-32 voxel units (2^-21 for cfg2); frames needing more than 2^-16 are refused.
     {
-        const double bound = std::ldexp(1.0, -33) * (double)(c.crop_w + c.crop_h + 1) + 1e-9;
-        const double target = 4.0 * bound * 4294967296.0;
+        const double qp2 = std::max(1.0, pose.qw * pose.qw + pose.qx * pose.qx +
+                                             pose.qy * pose.qy + pose.qz * pose.qz);
+        const double R = x.base_mm + norm3(pose.tx, pose.ty, pose.tz);
+        const double chain = 0x1p-44 * qp2 * x.qc2 * R / x.v;  // 512 * 2^-53
+        const double target = 4.0 * (x.coef_bound + chain) * 4294967296.0;
         int e = 4;
-        while (e < 16 && std::ldexp(1.0, e) < target) ++e;
+        for (double t = 16.0; e <= 16 && t < target; t *= 2.0) ++e;
+        if (e > 16)
+            return fail(SVR_E_INVALID, "pose too far from the grid origin for certified rounding "
+                        "(|t| / voxel ~ %.3g)", R / x.v);
         fp->tie_eps = 1u << e;
     }
     // image-plane normal in voxel space = third column of R_pose R_calib (k_pnn_plane table);
     // the plane passes through K (image origin).  z_c(x,y) = K_z - (n_x (x-K_x) + n_y (y-K_y))/n_z
     {
-        const long double nx = a.Mv[2], ny = a.Mv[5], nz = a.Mv[8];
-        const long double ax = std::fabs(nx), ay = std::fabs(ny), az = std::fabs(nz);
-        fp->plane_ok = (az > 0 && (ax + ay) < 0.99L * az) ? 1 : 0;  // 2h = s + 1.004 < 2
+        const double nx = a.Mv[2], ny = a.Mv[5], nz = a.Mv[8];
+        const double ax = std::fabs(nx), ay = std::fabs(ny), az = std::fabs(nz);
+        fp->plane_ok = (az > 0 && (ax + ay) < 0.99 * az) ? 1 : 0;  // 2h = s + 1.004 < 2
         if (fp->plane_ok) {
-            fp->pz[0] = (double)(a.K[2] + (nx * a.K[0] + ny * a.K[1]) / nz);
-            fp->pz[1] = (double)(-nx / nz);
-            fp->pz[2] = (double)(-ny / nz);
-            fp->pz[3] = (double)((ax + ay) / (2 * az) + 0.5L + 2e-3L);
+            fp->pz[0] = a.K[2] + (nx * a.K[0] + ny * a.K[1]) / nz;
+            fp->pz[1] = -nx / nz;
+            fp->pz[2] = -ny / nz;
+            fp->pz[3] = (ax + ay) / (2 * az) + 0.5 + 2e-3;
         } else {
             fp->pz[0] = fp->pz[1] = fp->pz[2] = fp->pz[3] = 0.0;
         }
@@ -262,15 +307,15 @@ static int make_params(const svr_rigid& pose, const svr_calib& c, const svr_grid
 // Conservative box (global indices) a frame can touch: affine extremes at the image corners
 // (linear) or at every scanline's end samples (fan), widened by one voxel.
 static svr_box frame_box(const svr_grid_desc& g, const svr_calib& c, const svr_rigid& pose) {
-    Affine a = frame_affine(pose, c, g);
-    long double lo[3], hi[3];
+    Affine a = frame_affine(pose, prep_ctx(c, g));
+    double lo[3], hi[3];
     for (int k = 0; k < 3; ++k) {
-        lo[k] = std::numeric_limits<long double>::infinity();
+        lo[k] = std::numeric_limits<double>::infinity();
         hi[k] = -lo[k];
     }
-    auto add = [&](long double px, long double py) {
+    auto add = [&](double px, double py) {
         for (int k = 0; k < 3; ++k) {
-            long double u = a.K[k] + a.Mv[3 * k] * px + a.Mv[3 * k + 1] * py;
+            double u = a.K[k] + a.Mv[3 * k] * px + a.Mv[3 * k + 1] * py;
             lo[k] = std::min(lo[k], u);
             hi[k] = std::max(hi[k], u);
         }
@@ -278,15 +323,15 @@ static svr_box frame_box(const svr_grid_desc& g, const svr_calib& c, const svr_r
     if (c.probe == SVR_PROBE_FAN) {
         std::vector<double> s, co;
         fan_table(c, s, co);
-        const long double dr = ((long double)c.fan_r1_mm - c.fan_r0_mm) / c.crop_w;
-        const long double ra = c.fan_r0_mm + 0.5L * dr, rb = c.fan_r0_mm + (c.crop_w - 0.5L) * dr;
+        const double dr = ((double)c.fan_r1_mm - c.fan_r0_mm) / c.crop_w;
+        const double ra = c.fan_r0_mm + 0.5 * dr, rb = c.fan_r0_mm + (c.crop_w - 0.5) * dr;
         for (int i = 0; i < c.crop_h; ++i) {
             add(ra * s[i], ra * co[i]);
             add(rb * s[i], rb * co[i]);
         }
     } else {
-        const long double X = (long double)(c.crop_w - 1) * c.scale_x_mm;
-        const long double Y = (long double)(c.crop_h - 1) * c.scale_y_mm;
+        const double X = (double)(c.crop_w - 1) * c.scale_x_mm;
+        const double Y = (double)(c.crop_h - 1) * c.scale_y_mm;
         add(0, 0);
         add(X, 0);
         add(0, Y);
@@ -296,13 +341,13 @@ static svr_box frame_box(const svr_grid_desc& g, const svr_calib& c, const svr_r
     int b0[3], b1[3];
     bool empty = false;
     for (int k = 0; k < 3; ++k) {
-        long double l = std::floor(lo[k] + 0.5L) - 1, h = std::floor(hi[k] + 0.5L) + 1;
+        double l = std::floor(lo[k] + 0.5) - 1, h = std::floor(hi[k] + 0.5) + 1;
         if (!(h >= 0) || !(l <= n[k] - 1)) {
             empty = true;
             break;
         }
-        b0[k] = (int)std::max<long double>(l, 0);
-        b1[k] = (int)std::min<long double>(h, n[k] - 1);
+        b0[k] = (int)std::max<double>(l, 0);
+        b1[k] = (int)std::min<double>(h, n[k] - 1);
     }
     if (empty) return svr_box{1, 1, 1, 0, 0, 0};
     return svr_box{b0[0], b0[1], b0[2], b1[0], b1[1], b1[2]};
@@ -518,7 +563,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFree(v->d_stats);
     cudaFree(v->d_counter);
     cudaFree(v->d_params);
-    cudaFreeHost(v->h_params);
+    for (int i = 0; i < 2; ++i) cudaFreeHost(v->h_params[i]);
     cudaFree(v->d_boxes);
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
@@ -532,7 +577,8 @@ extern "C" int svr_destroy(svr_volume* v) {
         if (v->ev_free[i]) cudaEventDestroy(v->ev_free[i]);
         if (v->ev_h2d[i]) cudaEventDestroy(v->ev_h2d[i]);
     }
-    if (v->params_ev) cudaEventDestroy(v->params_ev);
+    for (int i = 0; i < 2; ++i)
+        if (v->params_ev[i]) cudaEventDestroy(v->params_ev[i]);
     if (v->own_stream && v->stream) cudaStreamDestroy(v->stream);
     if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
     cudaGetLastError();
@@ -581,7 +627,8 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     }
     if (e == cudaSuccess) e = cudaMalloc(&v->d_stats, sizeof(ull) * kStCount);
     if (e == cudaSuccess) e = cudaMalloc(&v->d_counter, sizeof(ull) * 2);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->params_ev, cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&v->params_ev[i], cudaEventDisableTiming);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&v->ev_ready[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_free[i], cudaEventDisableTiming);
@@ -646,19 +693,23 @@ extern "C" int svr_get_desc(const svr_volume* v, svr_grid_desc* out) {
     return SVR_OK;
 }
 
+// Select the host parameter buffer for this call (v->pslot); its previous upload, two calls
+// back, must have finished before it is rewritten.
 static int ensure_params(svr_volume* v, int n) {
-    // the previous upload from h_params must have finished before it is rewritten
-    CK(cudaEventSynchronize(v->params_ev));
+    v->pslot ^= 1;
+    CK(cudaEventSynchronize(v->params_ev[v->pslot]));
     if (n <= v->params_cap) return SVR_OK;
     int cap = std::max(n, 2 * v->params_cap);
     CK(cudaStreamSynchronize(v->stream));
     cudaFree(v->d_params);
-    cudaFreeHost(v->h_params);
     v->d_params = nullptr;
-    v->h_params = nullptr;
+    for (int i = 0; i < 2; ++i) {
+        cudaFreeHost(v->h_params[i]);
+        v->h_params[i] = nullptr;
+    }
     v->params_cap = 0;
     CK(cudaMalloc(&v->d_params, sizeof(FrameParams) * cap));
-    CK(cudaMallocHost(&v->h_params, sizeof(FrameParams) * cap));
+    for (int i = 0; i < 2; ++i) CK(cudaMallocHost(&v->h_params[i], sizeof(FrameParams) * cap));
     v->params_cap = cap;
     return SVR_OK;
 }
@@ -920,13 +971,15 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
     if (n > 1 && fstride < pitch * (h - 1) + w)
         return fail(SVR_E_INVALID, "frame stride %lld too small", (long long)fstride);
     if (int e = ensure_params(v, n)) return e;
+    const PrepCtx ctx = prep_ctx(*c, v->d);
+    FrameParams* hp = v->h_params[v->pslot];
     for (int k = 0; k < n; ++k)
-        if (int e = make_params(poses[k], *c, v->d, &v->h_params[k]))
+        if (int e = make_params(poses[k], ctx, c->scale_x_mm, c->scale_y_mm, &hp[k]))
             return fail(e, "frame %d: %s", k, g_err.c_str());
     if (int e = ensure_fan(v, *c)) return e;
-    CK(cudaMemcpyAsync(v->d_params, v->h_params, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
+    CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
                        v->stream));
-    CK(cudaEventRecord(v->params_ev, v->stream));
+    CK(cudaEventRecord(v->params_ev[v->pslot], v->stream));
     const DevCalib cal = dev_calib(*c);
     int* boxes = nullptr;
     if (want_box) {
