@@ -91,6 +91,7 @@ struct svr_volume {
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
+    int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 closed form, 0 carries
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
     int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
 };
@@ -597,6 +598,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     v->d = *desc;
     if (const char* e = std::getenv("SVR_FILL_KERNEL")) v->fill_smem = !std::strcmp(e, "smem");
     if (const char* e = std::getenv("SVR_FILL_ZC")) v->fill_zc = std::atoi(e);
+    if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
                            : !std::strcmp(e, "tile")   ? 2
@@ -883,7 +885,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     TileShape ts;
     const bool tile = mode == kModeInsert && v->insert_kernel == 2 && tile_ok(v, cal, w, h, &ts, 8);
     const bool plane = mode == kModeInsert && v->insert_kernel == 3 && !skip && w >= 4 * kChunk &&
-                       tile_ok(v, cal, w, h, &ts, 4);
+                       (long long)v->d.nx * v->d.ny < (1ll << 22) && tile_ok(v, cal, w, h, &ts, 4);
     const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
@@ -900,17 +902,25 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             const int ntx = (cpr + kPlaneTW - 1) / kPlaneTW, nty = (h + kPlaneTH - 1) / kPlaneTH;
             dim3 grid(ntx, m, nty);
             const GridDev gd = dev_grid(v->d);
-#define LP(a, b)                                                                                  \
-    k_pnn_plane<a, b><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,      \
-                                                   v->d_fan, gd, v->acc, bx, stats, v->d_work,     \
-                                                   v->d_work_n, v->work_cap);                      \
+#define LP(a, b, c)                                                                               \
+    k_pnn_plane<a, b, c><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,   \
+                                                      v->d_fan, gd, v->acc, bx, stats, v->d_work,  \
+                                                      v->d_work_n, v->work_cap, 1u << 20);         \
     k_pnn_work<a, b><<<4096, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,     \
                                                      gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
                                                      v->work_cap)
-            if (vec) {
-                if (box) { LP(true, true); } else { LP(true, false); }
+            if (v->plane_walk) {
+                if (vec) {
+                    if (box) { LP(true, true, 1); } else { LP(true, false, 1); }
+                } else {
+                    if (box) { LP(false, true, 1); } else { LP(false, false, 1); }
+                }
             } else {
-                if (box) { LP(false, true); } else { LP(false, false); }
+                if (vec) {
+                    if (box) { LP(true, true, 0); } else { LP(true, false, 0); }
+                } else {
+                    if (box) { LP(false, true, 0); } else { LP(false, false, 0); }
+                }
             }
 #undef LP
             v->launches += 2;
