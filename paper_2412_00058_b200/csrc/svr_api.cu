@@ -91,9 +91,12 @@ struct svr_volume {
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
-    int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 closed form, 0 carries
+    int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 step counters, 0 carries
+    int plane_prefetch = 1;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk's voxel lines
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
     int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
+    int fill_depth = 1;         // SVR_FILL_DEPTH: planes in flight per warp in k_fill_warp (1/2)
+    int fill_ty = 8;            // SVR_FILL_TY: y rows per warp in k_fill_warp (4/8/12/16)
 };
 
 // ---------------------------------------------------------------- host geometry (exact)
@@ -598,7 +601,13 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     v->d = *desc;
     if (const char* e = std::getenv("SVR_FILL_KERNEL")) v->fill_smem = !std::strcmp(e, "smem");
     if (const char* e = std::getenv("SVR_FILL_ZC")) v->fill_zc = std::atoi(e);
+    if (const char* e = std::getenv("SVR_FILL_DEPTH")) v->fill_depth = std::atoi(e) == 1 ? 1 : 2;
+    if (const char* e = std::getenv("SVR_FILL_TY")) {
+        const int t = std::atoi(e);
+        v->fill_ty = (t == 4 || t == 12 || t == 16) ? t : 8;
+    }
     if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::atoi(e) ? 1 : 0;
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
                            : !std::strcmp(e, "tile")   ? 2
@@ -905,7 +914,8 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
 #define LP(a, b, c)                                                                               \
     k_pnn_plane<a, b, c><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,   \
                                                       v->d_fan, gd, v->acc, bx, stats, v->d_work,  \
-                                                      v->d_work_n, v->work_cap, 1u << 20);         \
+                                                      v->d_work_n, v->work_cap, 1u << 20,          \
+                                                      v->plane_prefetch);                          \
     k_pnn_work<a, b><<<4096, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,     \
                                                      gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
                                                      v->work_cap)
@@ -1146,7 +1156,7 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
             BoxTiles t;
             t.b = b;
             t.ntx = (b.x1 - b.x0 + 1 + 119) / 120;
-            t.nty = (b.y1 - b.y0 + 1 + 7) / 8;
+            t.nty = (b.y1 - b.y0 + 1 + v->fill_ty - 1) / v->fill_ty;
             t.first = total;
             total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
             bt.push_back(t);
@@ -1156,9 +1166,24 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         const dim3 grd = grid_1d(total);
         const BoxTiles* dt = (const BoxTiles*)d;
         const int nb = (int)bt.size();
-        if (zc == 8) k_fill_warp<8><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter);
-        else if (zc == 32) k_fill_warp<32><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter);
-        else k_fill_warp<16><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter);
+#define FW(Z, D, T) k_fill_warp<Z, D, T><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter)
+        const int ty = v->fill_ty;
+        if (v->fill_depth == 2) {
+            if (zc == 8) FW(8, 2, 8);
+            else if (zc == 32) FW(32, 2, 8);
+            else FW(16, 2, 8);
+        } else if (ty == 4) {
+            FW(16, 1, 4);
+        } else if (ty == 12) {
+            FW(16, 1, 12);
+        } else if (ty == 16) {
+            FW(16, 1, 16);
+        } else {
+            if (zc == 8) FW(8, 1, 8);
+            else if (zc == 32) FW(32, 1, 8);
+            else FW(16, 1, 8);
+        }
+#undef FW
         v->launches++;
         CKL();
         return SVR_OK;

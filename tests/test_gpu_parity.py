@@ -229,13 +229,22 @@ def test_footprint_counts():
         assert u[k] == int((r.count > 0).sum())
 
 
+INSERT_KERNELS = ["plane", "plane-carry", "direct", "rows", "tile"]
+
+
+def _select_kernel(monkeypatch, kernel):
+    """SVR_INSERT_KERNEL (+ SVR_PLANE_WALK=0 for the carry-walk form of k_pnn_plane)."""
+    monkeypatch.setenv("SVR_INSERT_KERNEL", kernel.split("-")[0])
+    monkeypatch.setenv("SVR_PLANE_WALK", "0" if kernel == "plane-carry" else "1")
+
+
 @pytest.mark.parametrize("name", ["small_linear", "small_fan"])
-@pytest.mark.parametrize("kernel", ["plane", "direct", "rows", "tile"])
+@pytest.mark.parametrize("kernel", INSERT_KERNELS)
 def test_golden_fixtures_gpu(name, kernel, monkeypatch):
     """CUDA path against the committed fixtures (accumulators from the reference's own
     pixel_to_world, tests/golden/make_golden.py) for every insert kernel variant."""
     from golden_util import Fixture
-    monkeypatch.setenv("SVR_INSERT_KERNEL", kernel)
+    _select_kernel(monkeypatch, kernel)
     fx = Fixture(name)
     grid = pkg.VoxelGrid(fx.dims, fx.voxel_mm, fx.origin, device=0)
     boxes, _ = grid.insert_frames(fx.frames, fx.poses, fx.calib, want_boxes=True)
@@ -257,9 +266,9 @@ def test_golden_fixtures_gpu(name, kernel, monkeypatch):
     assert np.array_equal(s0, fx["sum_skip0"]) and np.array_equal(c0, fx["count_skip0"])
 
 
-@pytest.mark.parametrize("kernel", ["plane", "direct", "rows", "tile"])
+@pytest.mark.parametrize("kernel", INSERT_KERNELS)
 def test_cfg1_all_kernels(kernel, monkeypatch):
-    monkeypatch.setenv("SVR_INSERT_KERNEL", kernel)
+    _select_kernel(monkeypatch, kernel)
     wl = synth.cfg1()
     frames = wl.frames_np()
     grid = _grid(wl)
