@@ -119,13 +119,18 @@ const char* svr_last_error(void);
 /* number of visible CUDA devices (0 on a CPU-only host; never fails) */
 int svr_device_count(void);
 
-/* RigidTransform::from_matrix4 (geometry.hpp:245-251 -> Shepperd from_matrix3 :173-190). */
+/* RigidTransform::from_matrix4 (geometry.hpp:133-139 -> Shepperd from_matrix3 :61-78). */
 int svr_pose_from_matrix4(const double m[16], svr_rigid* out);
-/* compose (geometry.hpp:254-256) */
+/* compose (geometry.hpp:142-144) */
 int svr_compose(const svr_rigid* a, const svr_rigid* b, svr_rigid* out);
-/* interpolate_pose (geometry.hpp:306-321), poses sorted by t_ms. */
+/* interpolate_pose (geometry.hpp:194-209, slerp :82-100), poses sorted by t_ms. */
 int svr_interpolate_pose(const double* t_ms, const svr_rigid* poses, int n, double t, svr_rigid* out);
-/* pixel_to_world (geometry.hpp:291-297) for the linear probe, fan point for SVR_PROBE_FAN. */
+/* Ingest pose matching: out[k] = interpolate_pose(poses, frame_t_ms[k] - latency_ms) for the m
+ * frames; valid[k] = 0 (identity pose) where that time lies outside the sampled span. */
+int svr_match_poses(const double* pose_t_ms, const svr_rigid* poses, int32_t n,
+                    const double* frame_t_ms, int32_t m, double latency_ms, svr_rigid* out,
+                    uint8_t* valid, int32_t* n_valid);
+/* pixel_to_world (geometry.hpp:179-185) for the linear probe, fan point for SVR_PROBE_FAN. */
 int svr_pixel_to_world(double col, double row, const svr_calib* calib, const svr_rigid* pose,
                        double out_mm[3]);
 /* Conservative voxel box a frame can touch (routing to z-slabs); clipped to the global grid. */
@@ -191,6 +196,14 @@ int svr_read_accumulators(svr_volume* vol, const svr_box* box, uint32_t* sum_out
                           uint16_t* count_out);
 /* VoxelGrid::value = round(sum/count); apply_fills adds rounded fill values. */
 int svr_read_values(svr_volume* vol, const svr_box* box, int32_t apply_fills, uint8_t* out);
+/* export_slices along x: nx images of ny x nzl u8 values (row = z, column =
+ * y), out[(x * nzl + z) * ny + y]; values as svr_read_values.  out may be host or device. */
+int svr_export_slices_x(svr_volume* vol, int32_t apply_fills, uint8_t* out);
+/* export_slices to files: dir/<x zero-padded to `digits`>.pgm (binary P5, image.hpp:34-42). */
+int svr_export_slices(svr_volume* vol, const char* dir, int32_t apply_fills, int32_t digits,
+                      int32_t* files_out);
+/* Volume file: raw u8 values of the slab, x fastest then y then z. */
+int svr_export_volume(svr_volume* vol, const char* path, int32_t apply_fills);
 /* raw fill layer: (n << 16) | payload (mean: sum of neighbour values; median: value). */
 int svr_read_fill(svr_volume* vol, const svr_box* box, uint32_t* out);
 /* trilinear volumes: f32 weighted sum and weight */
@@ -211,6 +224,26 @@ int svr_count_footprint(svr_volume* vol, const uint8_t* px, int64_t row_pitch,
 int svr_synth_frames(void* dst, int32_t w, int32_t h, int32_t first_frame, int32_t nframes,
                      const svr_calib* calib, const svr_rigid* poses, int32_t kind, uint64_t seed,
                      int device, void* cuda_stream);
+
+/* ---------------------------------------------------------------- ingest (host) ---- */
+/* read_pgm header (image.hpp:44-66): binary P5, '#' comments, maxval 255.  Unreadable file ->
+ * SVR_E_IO; not P5 / malformed / maxval != 255 -> SVR_E_INVALID (core.hpp:19-32). */
+int svr_pgm_info(const char* path, int32_t* width, int32_t* height);
+/* read_pgm (image.hpp:44-72) into out (row pitch >= width); dims must match the file. */
+int svr_pgm_read(const char* path, uint8_t* out, int64_t row_pitch, int32_t width, int32_t height);
+/* write_pgm (image.hpp:34-42). */
+int svr_pgm_write(const char* path, const uint8_t* px, int64_t row_pitch, int32_t width,
+                  int32_t height);
+/* ScanBundle frame loader: decode n PGM files of raw_w x raw_h with nthreads
+ * threads (<= 0: all cores), applying crop = {x, y, w, h} (ImageCalibration::crop_rect,
+ * geometry.hpp:156-158) while decoding (NULL = whole frame), into out + k * frame_stride with row
+ * pitch = cropped width (e.g. a pinned staging buffer for svr_insert_frames).  The lowest failing
+ * index is reported in *failed_index and named in svr_last_error. */
+int svr_load_frames(const char* const* paths, int32_t n, int32_t raw_w, int32_t raw_h,
+                    const int32_t* crop, uint8_t* out, int64_t frame_stride, int32_t nthreads,
+                    int32_t* failed_index);
+/* Write nbytes to a new file (volume files). */
+int svr_write_raw(const char* path, const uint8_t* data, int64_t nbytes);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,7 @@ class OrcGrid(C.Structure):
                 ("sum", C.c_void_p), ("count", C.c_void_p), ("fill", C.c_void_p),
                 ("wsum", C.c_void_p), ("weight", C.c_void_p),
                 ("frames", C.c_uint64), ("inserted", C.c_uint64), ("oob", C.c_uint64),
-                ("skipped_zero", C.c_uint64), ("saturated", C.c_uint64)]
+                ("skipped_zero", C.c_uint64), ("saturated", C.c_uint64), ("fill_mode", C.c_int32)]
 
 
 _lib = None
@@ -75,6 +75,9 @@ def ref():
         R.ref_compose.argtypes = [PR, PR, PR]
         R.ref_apply.argtypes = [PR, PD, PD]
         R.ref_interpolate_pose.argtypes = [PD, PR, C.c_int, C.c_double, PR]
+        R.ref_read_pgm.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int32)]
+        R.ref_write_pgm.argtypes = [C.c_char_p, C.c_void_p, C.c_int32, C.c_int32]
         R.ref_median_lower.argtypes = [PD, C.c_int]
         R.ref_median_lower.restype = C.c_double
         R.ref_insert_frames.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, PD,

@@ -1,5 +1,5 @@
 // ref_shim.cpp — C entry points over the REFERENCE's own headers
-// (/root/reference/proj/include/spinevol/{core,geometry}.hpp), compiled in place by
+// (/root/reference/proj/include/spinevol/{core,geometry,image}.hpp), compiled in place by
 // oracle/Makefile into oracle/_ref/libspinevol_ref.so.  TEST INFRASTRUCTURE ONLY:
 // it pins the C restatement (svr_oracle.c) and serves as the "reference" CPU baseline.
 //
@@ -16,6 +16,7 @@
 
 #include "spinevol/core.hpp"
 #include "spinevol/geometry.hpp"
+#include "spinevol/image.hpp"
 #include "../include/spinevol_b200.h"
 
 using namespace spinevol;
@@ -177,6 +178,34 @@ int ref_insert_frames(int32_t nx, int32_t ny, int32_t z_begin, int32_t z_end, do
     for (auto& t : th) t.join();
     if (inserted_out) *inserted_out = total.load();
     return 0;
+}
+
+// read_pgm / write_pgm (image.hpp:34-72).  Returns 0, 2 (InvalidInput) or 4 (IoError);
+// ref_read_pgm copies at most cap bytes and reports the dims.
+int ref_read_pgm(const char* path, uint8_t* out, int64_t cap, int32_t* w, int32_t* h) {
+    try {
+        Image8 img = read_pgm(path);
+        *w = img.width;
+        *h = img.height;
+        const int64_t n = std::min<int64_t>(cap, (int64_t)img.data.size());
+        if (n > 0) std::copy(img.data.begin(), img.data.begin() + n, out);
+        return 0;
+    } catch (const InvalidInput&) {
+        return 2;
+    } catch (const IoError&) {
+        return 4;
+    }
+}
+
+int ref_write_pgm(const char* path, const uint8_t* px, int32_t w, int32_t h) {
+    try {
+        Image8 img(w, h);
+        std::copy(px, px + (size_t)w * h, img.data.begin());
+        write_pgm(img, path);
+        return 0;
+    } catch (const IoError&) {
+        return 4;
+    }
 }
 
 }  // extern "C"

@@ -304,6 +304,7 @@ static int cmp_u32(const void* a, const void* b) {
  * Returns the number of filled voxels. */
 int64_t orc_fill_holes(orc_grid* g, const svr_box* region, int32_t mode, int32_t radius) {
     svr_box b;
+    g->fill_mode = mode;
     if (region) {
         b = *region;
     } else {
@@ -390,8 +391,8 @@ void orc_values(const orc_grid* g, int32_t apply_fills, uint8_t* out) {
             out[i] = (uint8_t)voxel_value(g->sum[i], c);
         } else if (apply_fills && g->fill && (g->fill[i] >> 16)) {
             uint32_t nn = g->fill[i] >> 16, s = g->fill[i] & 0xFFFFu;
-            /* mean fills round like value(): (2s+n)/(2n) */
-            out[i] = (uint8_t)((2u * s + nn) / (2u * nn));
+            /* mean fills round like value(): (2s+n)/(2n); median fills carry the value */
+            out[i] = g->fill_mode == SVR_FILL_MEAN ? (uint8_t)((2u * s + nn) / (2u * nn)) : (uint8_t)s;
         } else {
             out[i] = 0;
         }
@@ -533,7 +534,7 @@ void orc_coronal_projection(const orc_grid* g, int32_t mode, int32_t axis, int32
                     v = voxel_value(g->sum[lin], cnt);
                 } else if (use_fills && g->fill && (g->fill[lin] >> 16)) {
                     uint32_t nn = g->fill[lin] >> 16, sm = g->fill[lin] & 0xFFFFu;
-                    v = (2u * sm + nn) / (2u * nn);
+                    v = g->fill_mode == SVR_FILL_MEAN ? (2u * sm + nn) / (2u * nn) : sm;
                 } else {
                     continue;
                 }

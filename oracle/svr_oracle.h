@@ -36,6 +36,7 @@ typedef struct orc_grid {
     float* wsum;              /* trilinear mode (may be NULL) */
     float* weight;
     uint64_t frames, inserted, oob, skipped_zero, saturated;
+    int32_t fill_mode;        /* mode of the latest orc_fill_holes (decodes the fill layer) */
 } orc_grid;
 
 /* geometry */

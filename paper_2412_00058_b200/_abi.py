@@ -117,6 +117,16 @@ SIGNATURES = {
     "svr_get_stats": (C.c_int, [P, PS]),
     "svr_count_footprint": (C.c_int, [P, P, I64, I64, I32, I32, I32, PR, PC, I32, C.POINTER(I64)]),
     "svr_synth_frames": (C.c_int, [P, I32, I32, I32, I32, PC, PR, I32, U64, C.c_int, P]),
+    "svr_export_slices_x": (C.c_int, [P, I32, P]),
+    "svr_export_slices": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(I32)]),
+    "svr_export_volume": (C.c_int, [P, C.c_char_p, I32]),
+    "svr_pgm_info": (C.c_int, [C.c_char_p, C.POINTER(I32), C.POINTER(I32)]),
+    "svr_pgm_read": (C.c_int, [C.c_char_p, P, I64, I32, I32]),
+    "svr_pgm_write": (C.c_int, [C.c_char_p, P, I64, I32, I32]),
+    "svr_load_frames": (C.c_int, [C.POINTER(C.c_char_p), I32, I32, I32, C.POINTER(I32), P, I64, I32,
+                                  C.POINTER(I32)]),
+    "svr_write_raw": (C.c_int, [C.c_char_p, P, I64]),
+    "svr_match_poses": (C.c_int, [C.POINTER(D), PR, I32, C.POINTER(D), I32, D, PR, P, C.POINTER(I32)]),
 }
 
 _lib = None

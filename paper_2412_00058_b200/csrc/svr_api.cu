@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "svr_host.hpp"
 #include "svr_kernels.cuh"
 
 using namespace svr;
@@ -20,6 +21,16 @@ using namespace svr;
 static thread_local std::string g_err;
 
 static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int svr_fail(int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
     va_start(ap, fmt);
@@ -95,6 +106,7 @@ struct svr_volume {
     int plane_prefetch = 1;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk's voxel lines
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
     int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
+    int fill_mode = SVR_FILL_MEAN;  // mode of the latest fill_holes: decodes the fill layer on readout
     int fill_depth = 1;         // SVR_FILL_DEPTH: planes in flight per warp in k_fill_warp (1/2)
     int fill_ty = 8;            // SVR_FILL_TY: y rows per warp in k_fill_warp (4/8/12/16)
 };
@@ -401,7 +413,7 @@ extern "C" int svr_pose_from_matrix4(const double m[16], svr_rigid* out) {
     if (std::abs(m[12]) > 1e-9 || std::abs(m[13]) > 1e-9 || std::abs(m[14]) > 1e-9 ||
         std::abs(m[15] - 1.0) > 1e-9)
         return fail(SVR_E_INVALID, "bottom row of homogeneous matrix must be 0 0 0 1");
-    // Shepperd's method (geometry.hpp:173-190) on the row-major rotation block
+    // Shepperd's method (geometry.hpp:61-78) on the row-major rotation block
     const double r[9] = {m[0], m[1], m[2], m[4], m[5], m[6], m[8], m[9], m[10]};
     double tr = r[0] + r[4] + r[8];
     double q[4];
@@ -427,7 +439,7 @@ extern "C" int svr_pose_from_matrix4(const double m[16], svr_rigid* out) {
 
 extern "C" int svr_compose(const svr_rigid* a, const svr_rigid* b, svr_rigid* out) {
     if (!a || !b || !out) return fail(SVR_E_INVALID, "NULL argument");
-    // compose (geometry.hpp:254-256): rotation (a.q * b.q).normalized(), translation a.apply(b.t)
+    // compose (geometry.hpp:142-144): rotation (a.q * b.q).normalized(), translation a.apply(b.t)
     double q[4] = {a->qw * b->qw - a->qx * b->qx - a->qy * b->qy - a->qz * b->qz,
                    a->qw * b->qx + a->qx * b->qw + a->qy * b->qz - a->qz * b->qy,
                    a->qw * b->qy - a->qx * b->qz + a->qy * b->qw + a->qz * b->qx,
@@ -443,7 +455,7 @@ extern "C" int svr_compose(const svr_rigid* a, const svr_rigid* b, svr_rigid* ou
 
 extern "C" int svr_interpolate_pose(const double* t_ms, const svr_rigid* poses, int n, double t,
                                     svr_rigid* out) {
-    // interpolate_pose (geometry.hpp:306-321) + slerp (:194-212)
+    // interpolate_pose (geometry.hpp:194-209) + slerp (:82-100)
     if (!t_ms || !poses || !out || n <= 0) return fail(SVR_E_INVALID, "empty pose sequence");
     if (t < t_ms[0] || t > t_ms[n - 1])
         return fail(SVR_E_INVALID, "pose interpolation time outside sampled range");
@@ -479,6 +491,34 @@ extern "C" int svr_interpolate_pose(const double* t_ms, const svr_rigid* poses, 
     q_normalize(q);
     r.qw = q[0]; r.qx = q[1]; r.qy = q[2]; r.qz = q[3];
     *out = r;
+    return SVR_OK;
+}
+
+// Frame/pose matching of the ingest front-end (SPEC.md geometry "Pose/frame matching"): each
+// frame time shifted by -latency_ms, then interpolate_pose.  Frames whose shifted time falls
+// outside the sampled span (where interpolate_pose throws) get valid = 0 and an identity pose.
+extern "C" int svr_match_poses(const double* pose_t_ms, const svr_rigid* poses, int32_t n,
+                               const double* frame_t_ms, int32_t m, double latency_ms,
+                               svr_rigid* out, uint8_t* valid, int32_t* n_valid) {
+    if (m < 0 || (m > 0 && (!frame_t_ms || !out || !valid))) return fail(SVR_E_INVALID, "invalid frame list");
+    if (n <= 0 || !pose_t_ms || !poses) return fail(SVR_E_INVALID, "empty pose sequence");
+    for (int i = 1; i < n; ++i)
+        if (!(pose_t_ms[i] >= pose_t_ms[i - 1]))
+            return fail(SVR_E_INVALID, "pose timestamps must be non-decreasing (sample %d)", i);
+    int nv = 0;
+    const std::string saved = g_err;
+    for (int k = 0; k < m; ++k) {
+        const double t = frame_t_ms[k] - latency_ms;
+        valid[k] = 0;
+        out[k] = svr_rigid{1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (!(t >= pose_t_ms[0] && t <= pose_t_ms[n - 1])) continue;
+        if (svr_interpolate_pose(pose_t_ms, poses, n, t, &out[k]) == SVR_OK) {
+            valid[k] = 1;
+            ++nv;
+        }
+    }
+    g_err = saved;
+    if (n_valid) *n_valid = nv;
     return SVR_OK;
 }
 
@@ -1216,6 +1256,9 @@ static int check_fill_args(svr_volume* v, int32_t mode, int32_t radius) {
     if (!v->acc) return fail(SVR_E_INVALID, "fill_holes needs a PNN volume");
     if (mode != SVR_FILL_MEAN && mode != SVR_FILL_MEDIAN) return fail(SVR_E_INVALID, "unknown fill mode");
     if (radius < 1 || radius > 8) return fail(SVR_E_INVALID, "fill radius must be in [1,8]");
+    // the mean fill code carries the neighbour sum in 16 bits: (2r+1)^3 - 1 neighbours of <= 255
+    // fit for r <= 2 (31620), not beyond
+    if (mode == SVR_FILL_MEAN && radius > 2) return fail(SVR_E_INVALID, "mean fill supports radius <= 2");
     if (mode == SVR_FILL_MEAN && (2 * radius + 1) * (2 * radius + 1) * (2 * radius + 1) * 255 > 65535)
         return fail(SVR_E_INVALID, "mean fill radius too large for the 16-bit fill payload");
     return SVR_OK;
@@ -1238,6 +1281,7 @@ extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode
     Box b;
     const bool any = clip_box(v, region, &b);
     if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
+    v->fill_mode = mode;
     if (any)
         if (int e = fill_boxes(v, std::vector<Box>{b}, mode, radius)) return e;
     return finish_count(v, filled_out);
@@ -1254,6 +1298,7 @@ extern "C" int svr_fill_holes_boxes(svr_volume* v, const svr_box* regions, int32
         if (clip_box(v, &regions[i], &b)) bs.push_back(b);
     }
     if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
+    v->fill_mode = mode;
     if (!bs.empty())
         if (int e = fill_boxes(v, bs, mode, radius)) return e;
     return finish_count(v, filled_out);
@@ -1384,7 +1429,7 @@ extern "C" int svr_coronal_projection(svr_volume* v, int32_t mode, int32_t axis,
     uint8_t* tmp = nullptr;
     CK(cudaMallocAsync(&tmp, n, v->stream));
     k_project<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, dev_grid(v->d), axis,
-                                                                 mode, use_fills, tmp);
+                                                                 mode, use_fills, v->fill_mode, tmp);
     v->launches++;
     CKL();
     CK(cudaMemcpyAsync(out, tmp, n, cudaMemcpyDefault, v->stream));
@@ -1445,13 +1490,58 @@ extern "C" int svr_read_values(svr_volume* v, const svr_box* box, int32_t apply_
     uint8_t* t = nullptr;
     CK(cudaMallocAsync(&t, n, v->stream));
     k_read_values<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, dev_grid(v->d), b,
-                                                                     apply_fills, t);
+                                                                     apply_fills, v->fill_mode, t);
     v->launches++;
     CKL();
     CK(cudaMemcpyAsync(out, t, n, cudaMemcpyDefault, v->stream));
     CK(cudaFreeAsync(t, v->stream));
     CK(cudaStreamSynchronize(v->stream));
     return SVR_OK;
+}
+
+extern "C" int svr_export_slices_x(svr_volume* v, int32_t apply_fills, uint8_t* out) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "not a PNN volume");
+    if (!out) return fail(SVR_E_INVALID, "out is NULL");
+    const GridDev g = dev_grid(v->d);
+    const long long n = (long long)g.nx * g.ny * g.nzl;
+    uint8_t* t = nullptr;
+    CK(cudaMallocAsync(&t, n, v->stream));
+    const dim3 grd((g.nx + 31) / 32, (g.ny + 31) / 32, g.nzl);
+    k_slices_x<<<grd, dim3(32, 8), 0, v->stream>>>(v->acc, v->fill, g, apply_fills, v->fill_mode, t);
+    v->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(out, t, n, cudaMemcpyDefault, v->stream));
+    CK(cudaFreeAsync(t, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
+extern "C" int svr_export_slices(svr_volume* v, const char* dir, int32_t apply_fills, int32_t digits,
+                                 int32_t* files_out) {
+    VOL_CHECK(v);
+    if (!dir) return fail(SVR_E_INVALID, "directory is NULL");
+    if (digits < 1 || digits > 9) return fail(SVR_E_INVALID, "digits must be in [1,9]");
+    const GridDev g = dev_grid(v->d);
+    std::vector<uint8_t> h((size_t)g.nx * g.ny * g.nzl);
+    if (int e = svr_export_slices_x(v, apply_fills, h.data())) return e;
+    for (int x = 0; x < g.nx; ++x) {
+        char path[4096];
+        if (std::snprintf(path, sizeof path, "%s/%0*d.pgm", dir, digits, x) >= (int)sizeof path)
+            return fail(SVR_E_INVALID, "slice path too long");
+        if (int e = svr_pgm_write(path, h.data() + (size_t)x * g.ny * g.nzl, g.ny, g.ny, g.nzl)) return e;
+    }
+    if (files_out) *files_out = g.nx;
+    return SVR_OK;
+}
+
+extern "C" int svr_export_volume(svr_volume* v, const char* path, int32_t apply_fills) {
+    VOL_CHECK(v);
+    if (!path) return fail(SVR_E_INVALID, "path is NULL");
+    if (!v->acc) return fail(SVR_E_INVALID, "not a PNN volume");
+    std::vector<uint8_t> h((size_t)v->d.nx * v->d.ny * (v->d.z_end - v->d.z_begin));
+    if (int e = svr_read_values(v, nullptr, apply_fills, h.data())) return e;
+    return svr_write_raw(path, h.data(), (int64_t)h.size());
 }
 
 extern "C" int svr_read_fill(svr_volume* v, const svr_box* box, uint32_t* out) {

@@ -301,7 +301,7 @@ def _percentile(v, p):
 
 
 def pose_from_matrix4(m) -> Rigid:
-    """RigidTransform::from_matrix4 (geometry.hpp:245-251)."""
+    """RigidTransform::from_matrix4 (geometry.hpp:133-139)."""
     a = (C.c_double * 16)(*[float(x) for x in np.asarray(m, dtype=np.float64).reshape(16)])
     r = Rigid()
     check(lib().svr_pose_from_matrix4(a, C.byref(r)))
