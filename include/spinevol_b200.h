@@ -245,6 +245,34 @@ int svr_load_frames(const char* const* paths, int32_t n, int32_t raw_w, int32_t 
 /* Write nbytes to a new file (volume files). */
 int svr_write_raw(const char* path, const uint8_t* data, int64_t nbytes);
 
+/* ---------------------------------------------------------------- segment ---------- */
+/* cut_depth_alg1 (SPEC.md segment; Table I Step 4): K |p_c1 - p_cn - L/2| + D clamped to
+ * [0, axial_extent_mm] (ImageCalibration::axial_extent_mm, geometry.hpp:174). */
+int svr_cut_depth_alg1(double p_c1, double p_cn, double K, double D, double L,
+                       double axial_extent_mm, double* out);
+/* apply_cut rows kept: [ceil(cut/sy - 1e-9), floor((cut+band)/sy + 1e-9)] clipped to [0,h-1]
+ * (empty when r0 > r1: the whole frame is cut). */
+int svr_cut_rows(double cut_mm, double band_mm, double scale_y_mm, int32_t h, int32_t* r0,
+                 int32_t* r1);
+/* smooth_depths (Table II Step 3): linear gap bridging (edges: nearest valid), then a sliding
+ * median_lower (core.hpp:93-99) of `window` (odd >= 3) samples clipped at the ends.  All-gap
+ * input -> SVR_E_ALGO. */
+int svr_smooth_depths(const double* depths, const uint8_t* valid, int32_t n, int32_t window,
+                      double* out);
+/* bone_contour (Table II Step 2) for n device-resident frames: brightness threshold thr = the
+ * floor(pct * (w*h - 1))-th smallest pixel; with S(r) = I[r] + I[r+1] + I[r+2], each column is
+ * scanned bottom-up to its first window with S(r) >= 3 thr, a cortex hit iff >= shadow_rows rows
+ * lie below that window and S(r) - S(r+3) >= grad_levels; frame row = median_lower of the hit
+ * rows, or -1 (no contour) when fewer than min_valid_frac * w columns hit.  Depth = row * sy. */
+int svr_bone_contour(const uint8_t* px, int64_t row_pitch, int64_t frame_stride, int32_t w,
+                     int32_t h, int32_t n, double pct, int32_t grad_levels, int32_t shadow_rows,
+                     double min_valid_frac, int32_t* row_out, int32_t* valid_cols_out,
+                     int32_t* threshold_out, int32_t* col_rows_out, int device, void* cuda_stream);
+/* apply_cut in place on n device-resident frames: rows outside [row0[k], row1[k]] set to 0. */
+int svr_apply_cut(uint8_t* px, int64_t row_pitch, int64_t frame_stride, int32_t w, int32_t h,
+                  int32_t n, const int32_t* row0, const int32_t* row1, int device,
+                  void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,16 @@ def lib():
         L.orc_render.argtypes = [PG, PB, C.c_int32, C.POINTER(RenderParams), P, P, P, P]
         L.orc_render_ints.argtypes = [C.POINTER(RenderParams), C.c_double, C.c_int32] + [C.POINTER(C.c_int32)] * 4
         L.orc_coronal_projection.argtypes = [PG, C.c_int32, C.c_int32, C.c_int32, P]
+        L.orc_cut_depth_alg1.argtypes = [C.c_double] * 6
+        L.orc_cut_depth_alg1.restype = C.c_double
+        L.orc_cut_rows.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int32,
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.orc_apply_cut.argtypes = [P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32]
+        L.orc_bone_contour.argtypes = [P, C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                                       C.c_int32, C.c_double, P, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32)]
+        L.orc_bone_contour.restype = C.c_int32
+        L.orc_smooth_depths.argtypes = [P, P, C.c_int32, C.c_int32, P]
         L.orc_insert_trilinear.argtypes = [PG, P, C.c_int64, C.c_int32, C.c_int32, PR, PC, C.c_int32]
         _lib = L
     return _lib

@@ -600,3 +600,117 @@ int orc_insert_trilinear(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t 
     free(fc);
     return 0;
 }
+
+
+/* ------------------------------------------------------------------ segment */
+static double orc_median_lower(double* v, int n) {
+    /* median_lower (core.hpp:93-99): v[(n-1)/2] of the sorted sequence */
+    for (int i = 1; i < n; ++i) { /* insertion sort: windows and column lists are small */
+        double x = v[i];
+        int j = i - 1;
+        while (j >= 0 && v[j] > x) { v[j + 1] = v[j]; --j; }
+        v[j + 1] = x;
+    }
+    return v[(n - 1) / 2];
+}
+
+/* cut_depth_alg1 (Table I Step 4): K |p_c1 - p_cn - L/2| + D, clamped to [0, axial extent]. */
+double orc_cut_depth_alg1(double p_c1, double p_cn, double K, double D, double L,
+                          double axial_extent_mm) {
+    double c = K * fabs(p_c1 - p_cn - L / 2.0) + D;
+    if (c < 0.0) c = 0.0;
+    if (c > axial_extent_mm) c = axial_extent_mm;
+    return c;
+}
+
+/* apply_cut rows: [ceil(cut/sy - 1e-9), floor((cut+band)/sy + 1e-9)] clipped to the image
+ * (the 1e-9 keeps 30/0.1 -> 300 and 45/0.1 -> 450 of the SPEC example exact). */
+void orc_cut_rows(double cut_mm, double band_mm, double scale_y_mm, int32_t h, int32_t* r0,
+                  int32_t* r1) {
+    double a = ceil(cut_mm / scale_y_mm - 1e-9), b = floor((cut_mm + band_mm) / scale_y_mm + 1e-9);
+    if (a < 0) a = 0;
+    if (b > h - 1) b = h - 1;
+    *r0 = (int32_t)a;
+    *r1 = (int32_t)b;
+}
+
+void orc_apply_cut(uint8_t* px, int64_t pitch, int32_t w, int32_t h, int32_t r0, int32_t r1) {
+    for (int32_t r = 0; r < h; ++r)
+        if (r < r0 || r > r1) memset(px + r * pitch, 0, (size_t)w);
+}
+
+/* bone_contour (Table II Step 2), pinned: brightness threshold thr = the frame's pct_rank-th
+ * smallest pixel (0-based); with S(r) = I[r] + I[r+1] + I[r+2] (a 3-row window), each column is
+ * scanned upward from the bottom and stops at the first window with S(r) >= 3 thr (the first
+ * bright structure from below).  It is the cortex ("first strong dark-to-bright transition",
+ * SPEC design decision) iff at least shadow_rows rows lie below the window -- all of them in
+ * non-bright windows, the acoustic shadow -- and S(r) - S(r+3) >= grad_levels (the 3-row-mean
+ * step over a 3-row baseline, in levels).  Frame row = median_lower of the cortex rows; -1 when
+ * fewer than min_valid_frac * w columns have one. */
+int32_t orc_bone_contour(const uint8_t* px, int64_t pitch, int32_t w, int32_t h, int64_t pct_rank,
+                         int32_t grad_levels, int32_t shadow_rows, double min_valid_frac,
+                         int32_t* col_rows, int32_t* valid_cols, int32_t* bright_thr) {
+    int64_t hist[256] = {0};
+    for (int32_t r = 0; r < h; ++r)
+        for (int32_t c = 0; c < w; ++c) hist[px[r * pitch + c]]++;
+    int32_t thr = 255;
+    int64_t cum = 0;
+    for (int v = 0; v < 256; ++v) {
+        cum += hist[v];
+        if (cum > pct_rank) { thr = v; break; }
+    }
+    int32_t nv = 0;
+    double* rows = (double*)malloc(sizeof(double) * (size_t)(w > 0 ? w : 1));
+    for (int32_t c = 0; c < w; ++c) {
+        int32_t hit = -1;
+        for (int32_t r = h - 3; r >= 0; --r) {
+            int S = px[r * pitch + c] + px[(r + 1) * pitch + c] + px[(r + 2) * pitch + c];
+            if (S < 3 * thr) continue;
+            if (h - (r + 3) >= shadow_rows && r + 5 <= h - 1) {
+                int Sb = px[(r + 3) * pitch + c] + px[(r + 4) * pitch + c] + px[(r + 5) * pitch + c];
+                if (S - Sb >= grad_levels) hit = r;
+            }
+            break;
+        }
+        if (col_rows) col_rows[c] = hit;
+        if (hit >= 0) rows[nv++] = hit;
+    }
+    if (valid_cols) *valid_cols = nv;
+    if (bright_thr) *bright_thr = thr;
+    int32_t out = -1;
+    if (nv > 0 && !((double)nv < min_valid_frac * (double)w)) out = (int32_t)orc_median_lower(rows, nv);
+    free(rows);
+    return out;
+}
+
+/* smooth_depths (Table II Step 3): gaps bridged linearly between the nearest valid samples
+ * (a + (b - a) * ((i - ia) / (ib - ia))), leading / trailing gaps take the nearest valid value;
+ * then median_lower over [i - window/2, i + window/2] clipped to the series. */
+int orc_smooth_depths(const double* d, const uint8_t* valid, int32_t n, int32_t window, double* out) {
+    if (window < 3 || window % 2 == 0) return -2;
+    int32_t first = -1, last = -1;
+    for (int32_t i = 0; i < n; ++i)
+        if (valid[i]) { if (first < 0) first = i; last = i; }
+    if (first < 0) return -1;
+    double* g = (double*)malloc(sizeof(double) * (size_t)n);
+    int32_t prev = -1;
+    for (int32_t i = 0; i < n; ++i) {
+        if (valid[i]) { g[i] = d[i]; prev = i; continue; }
+        if (i < first) { g[i] = d[first]; continue; }
+        if (i > last) { g[i] = d[last]; continue; }
+        int32_t nx = i + 1;
+        while (!valid[nx]) ++nx;
+        double t = (double)(i - prev) / (double)(nx - prev);
+        g[i] = d[prev] + (d[nx] - d[prev]) * t;
+    }
+    int32_t hw = window / 2;
+    double* win = (double*)malloc(sizeof(double) * (size_t)window);
+    for (int32_t i = 0; i < n; ++i) {
+        int32_t a = i - hw < 0 ? 0 : i - hw, b = i + hw > n - 1 ? n - 1 : i + hw, m = 0;
+        for (int32_t k = a; k <= b; ++k) win[m++] = g[k];
+        out[i] = orc_median_lower(win, m);
+    }
+    free(win);
+    free(g);
+    return 0;
+}

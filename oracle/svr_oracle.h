@@ -72,6 +72,18 @@ void orc_coronal_projection(const orc_grid* g, int32_t mode, int32_t depth_axis,
 int orc_insert_trilinear(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
                          const svr_rigid* pose, const svr_calib* calib, int32_t skip_zero);
 
+/* segment (SPEC.md segment module; the reference implements none of it: parity unpinned
+ * except median_lower, core.hpp:93-99, which these use) */
+double orc_cut_depth_alg1(double p_c1, double p_cn, double K, double D, double L,
+                          double axial_extent_mm);
+void orc_cut_rows(double cut_mm, double band_mm, double scale_y_mm, int32_t h, int32_t* r0,
+                  int32_t* r1);
+void orc_apply_cut(uint8_t* px, int64_t pitch, int32_t w, int32_t h, int32_t r0, int32_t r1);
+int32_t orc_bone_contour(const uint8_t* px, int64_t pitch, int32_t w, int32_t h, int64_t pct_rank,
+                         int32_t grad_levels, int32_t shadow_rows, double min_valid_frac,
+                         int32_t* col_rows, int32_t* valid_cols, int32_t* bright_thr);
+int orc_smooth_depths(const double* d, const uint8_t* valid, int32_t n, int32_t window, double* out);
+
 #ifdef __cplusplus
 }
 #endif

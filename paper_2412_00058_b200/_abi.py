@@ -127,6 +127,11 @@ SIGNATURES = {
                                   C.POINTER(I32)]),
     "svr_write_raw": (C.c_int, [C.c_char_p, P, I64]),
     "svr_match_poses": (C.c_int, [C.POINTER(D), PR, I32, C.POINTER(D), I32, D, PR, P, C.POINTER(I32)]),
+    "svr_cut_depth_alg1": (C.c_int, [D, D, D, D, D, D, C.POINTER(D)]),
+    "svr_cut_rows": (C.c_int, [D, D, D, I32, C.POINTER(I32), C.POINTER(I32)]),
+    "svr_smooth_depths": (C.c_int, [P, P, I32, I32, P]),
+    "svr_bone_contour": (C.c_int, [P, I64, I64, I32, I32, I32, D, I32, I32, D, P, P, P, P, C.c_int, P]),
+    "svr_apply_cut": (C.c_int, [P, I64, I64, I32, I32, I32, P, P, C.c_int, P]),
 }
 
 _lib = None
