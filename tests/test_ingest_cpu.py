@@ -181,3 +181,13 @@ def test_calib_json_roundtrip_fan():
     assert c2.probe == _abi.PROBE_FAN and c2.fan_r1_mm == 150.0 and c2.latency_ms == 7.0
     for f in ("qw", "qx", "qy", "qz", "tx", "ty", "tz"):
         assert abs(getattr(c2.image_to_transducer, f) - getattr(c.image_to_transducer, f)) < 1e-12
+
+
+def test_cli_exit_codes_cpu(tmp_path):
+    """cli exit codes: invalid input 2, I/O 4; no GPU needed to fail early."""
+    from paper_2412_00058_b200 import cli
+    assert cli.main(["synth", "bundle", "--frames", "0", "--out", str(tmp_path / "b")]) == 2
+    assert cli.main(["reconstruct", "--bundle", str(tmp_path / "missing"), "--out", str(tmp_path / "v")]) == 4
+    assert cli.main(["project", "--out", str(tmp_path / "p.pgm")]) == 2
+    assert cli.main(["nonsense"]) == 2
+    assert cli.main(["project", "--volume", str(tmp_path / "none.raw"), "--out", str(tmp_path / "p.pgm")]) == 4
