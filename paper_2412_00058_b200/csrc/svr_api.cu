@@ -103,7 +103,7 @@ struct svr_volume {
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
     int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 step counters, 0 carries
-    int plane_prefetch = 1;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk's voxel lines
+    int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
     int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
     int fill_mode = SVR_FILL_MEAN;  // mode of the latest fill_holes: decodes the fill layer on readout
@@ -647,7 +647,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         v->fill_ty = (t == 4 || t == 12 || t == 16) ? t : 8;
     }
     if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
-    if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
                            : !std::strcmp(e, "tile")   ? 2

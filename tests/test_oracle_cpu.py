@@ -324,3 +324,4 @@ def test_two_rank_gloo_slab_sharding_matches_unsharded():
                            start_method="spawn")
         res = open(out).read()
     assert res.startswith("ok"), res
+
