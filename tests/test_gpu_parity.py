@@ -279,7 +279,7 @@ def test_cfg1_all_kernels(kernel, monkeypatch):
     assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
 
 
-@pytest.mark.parametrize("fill_kernel", ["warp", "smem"])
+@pytest.mark.parametrize("fill_kernel", ["tma", "warp", "smem"])
 def test_mean_fill_kernels_bitexact(fill_kernel, monkeypatch):
     """Both r=1 mean-fill kernels (register/shuffle and shared-memory separable) against the
     oracle on a region with grid-edge clipping."""
