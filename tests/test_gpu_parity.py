@@ -366,3 +366,40 @@ def test_cfg2_full_size_properties(monkeypatch):
         else:
             assert n == ref_n and np.array_equal(fl, ref_fill), kernel
         del g
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_sharded_bench_step_equals_unsharded(world):
+    """bench.py's per-rank step on the GPU (z-slab grids with ghosts, routed frames, per-chunk
+    dirty boxes, fill + render), ranks run one after another in this process: the owned planes'
+    accumulators and the owned coronal rows equal the unsharded run bit for bit."""
+    from paper_2412_00058_b200 import sharding
+    wl = synth.cfg2(nframes=300)
+    frames = np.stack([wl.frames_np(k, 1)[0] for k in range(0, 300, 1)])
+    rp = synth.render_params()
+    fill_r = wl.fill_radius
+
+    def run(z_range, idx):
+        boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+        g = _grid(wl, z_range=z_range)
+        g.insert_frames(frames[idx], wl.poses[idx], wl.calib)
+        g.fill_holes_boxes(sharding.chunk_boxes(boxes, idx, z_range, chunk=32, dilate=fill_r), fill_r,
+                           pkg.FILL_MEAN, count=False)
+        g.render_coronal_boxes(sharding.chunk_boxes(boxes, idx, z_range, chunk=32), rp, fill_r)
+        return g
+
+    full = run((0, wl.dims[2]), np.arange(300))
+    s_full, c_full = full.accumulators()
+    mean_f, max_f, dep_f = full.read_coronal()
+    slabs = sharding.plan_slabs(wl.dims[2], world, fill_r + rp.median_radius)
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    for sl in slabs:
+        idx = sharding.route(boxes, sl.alloc)
+        g = run(sl.alloc, idx)
+        o0, o1 = sl.owned
+        s, c = g.accumulators((0, 0, o0, wl.dims[0] - 1, wl.dims[1] - 1, o1 - 1))
+        assert np.array_equal(c, c_full[o0:o1]) and np.array_equal(s, s_full[o0:o1])
+        m, x, d = g.read_coronal(o0, o1 - 1)
+        assert np.array_equal(m, mean_f[o0:o1]) and np.array_equal(x, max_f[o0:o1])
+        assert np.array_equal(d, dep_f[o0:o1])
+        del g
