@@ -103,6 +103,8 @@ struct svr_volume {
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
     int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 step counters, 0 carries
+    int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
+    int plane_tw_cur = 4;       // the width chosen for the current insert call
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
     int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
@@ -655,6 +657,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         v->fill_ty = (t == 4 || t == 12 || t == 16) ? t : 8;
     }
     if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("SVR_PLANE_TW")) v->plane_tw = std::atoi(e) == 6 ? 6 : 4;
     if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
@@ -957,11 +960,18 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             }
             CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
             const int ntx = (cpr + kPlaneTW - 1) / kPlaneTW, nty = (h + kPlaneTH - 1) / kPlaneTH;
-            dim3 grid(ntx, m, nty);
+            dim3 grid(ntx, m, nty), grid6((cpr + 5) / 6, m, nty);
+            const int tw = v->plane_tw_cur;
             const GridDev gd = dev_grid(v->d);
 #define LP(a, b, c)                                                                               \
-    k_pnn_plane<a, b, c><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,   \
-                                                      v->d_fan, gd, v->acc, bx, stats, v->d_work,  \
+    if (tw == 6)                                                                                  \
+        k_pnn_plane<a, b, c, 6><<<grid6, 192, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0,\
+                                                          cal, v->d_fan, gd, v->acc, bx, stats,     \
+                                                          v->d_work, v->d_work_n, v->work_cap,      \
+                                                          1u << 20, v->plane_prefetch);             \
+    else                                                                                          \
+    k_pnn_plane<a, b, c, 4><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0,   \
+                                                      cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,  \
                                                       v->d_work_n, v->work_cap, 1u << 20,          \
                                                       v->plane_prefetch);                          \
     k_pnn_work<a, b><<<4096, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,     \
@@ -1045,6 +1055,19 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
         if (int e = make_params(poses[k], ctx, c->scale_x_mm, c->scale_y_mm, &hp[k]))
             return fail(e, "frame %d: %s", k, g_err.c_str());
     if (int e = ensure_fan(v, *c)) return e;
+    // k_pnn_plane tile width: 6 chunks (96 px) when every frame's tile stays within the 32 x 32
+    // voxel table (x extent over 96 columns + 64 rows, plus the +-1 margins), else 4
+    v->plane_tw_cur = 4;
+    if (v->plane_tw == 6 && c->probe != SVR_PROBE_FAN) {
+        double mx = 0.0, my = 0.0;
+        for (int k = 0; k < n; ++k) {
+            mx = std::max(mx, std::fabs((double)hp[k].Dc[0]) * 95.0 + std::fabs((double)hp[k].Dr[0]) * 63.0);
+            my = std::max(my, std::fabs((double)hp[k].Dc[1]) * 95.0 + std::fabs((double)hp[k].Dr[1]) * 63.0);
+        }
+        mx /= 4294967296.0;
+        my /= 4294967296.0;
+        if (std::ceil(mx) + 4 <= 32 && std::ceil(my) + 4 <= 32) v->plane_tw_cur = 6;
+    }
     CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
                        v->stream));
     CK(cudaEventRecord(v->params_ev[v->pslot], v->stream));

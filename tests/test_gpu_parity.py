@@ -229,13 +229,15 @@ def test_footprint_counts():
         assert u[k] == int((r.count > 0).sum())
 
 
-INSERT_KERNELS = ["plane", "plane-carry", "direct", "rows", "tile"]
+INSERT_KERNELS = ["plane", "plane-carry", "plane-tw6", "direct", "rows", "tile"]
 
 
 def _select_kernel(monkeypatch, kernel):
-    """SVR_INSERT_KERNEL (+ SVR_PLANE_WALK=0 for the carry-walk form of k_pnn_plane)."""
+    """SVR_INSERT_KERNEL (+ SVR_PLANE_WALK=0 for the carry-walk form of k_pnn_plane,
+    SVR_PLANE_TW=6 for its 96-px tiles)."""
     monkeypatch.setenv("SVR_INSERT_KERNEL", kernel.split("-")[0])
     monkeypatch.setenv("SVR_PLANE_WALK", "0" if kernel == "plane-carry" else "1")
+    monkeypatch.setenv("SVR_PLANE_TW", "6" if kernel == "plane-tw6" else "4")
 
 
 @pytest.mark.parametrize("name", ["small_linear", "small_fan"])
