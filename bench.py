@@ -374,25 +374,38 @@ def run_ours(args):
         h2d = n_my * px_frame + n_my * 224
         d2h = 2 * rows * wl.dims[0] * 4
 
-        # ---- per-frame incremental latency (insert -> fill(box+1) -> render(box)), rank-local
-        lat_dev, lat_wall = [], []
-        nl = min(args.latency_frames, n_my)
-        mid = max(0, n_my // 2 - nl // 2)
-        le = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
-        for j in range(nl):
-            k = mid + j
+        # ---- per-frame incremental latency (insert -> fill(box+1) -> render(box)), rank-local:
+        # the product path is svr_frame_step (one CUDA-graph replay per frame); the per-call
+        # sequence of the same kernels is timed beside it
+        def frame_latency(nl, first, graph):
+            le = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
+            wall = []
+            for j in range(nl):
+                k = first + j
+                torch.cuda.synchronize()
+                w = time.perf_counter()
+                le[j][0].record(stream)
+                if graph:
+                    grid.frame_step(frames[k], poses[k:k + 1], wl.calib, fill_r, rp)
+                else:
+                    grid.insert_frames(frames[k], poses[k:k + 1], wl.calib)
+                    b = boxes[int(mine[k])]
+                    grid.fill_holes(pkg.dilate(b, fill_r), fill_r, pkg.FILL_MEAN, count=False)
+                    grid.render_coronal(b, rp, fill_r)
+                le[j][1].record(stream)
+                stream.synchronize()
+                wall.append((time.perf_counter() - w) * 1e3)
             torch.cuda.synchronize()
-            w = time.perf_counter()
-            le[j][0].record(stream)
-            grid.insert_frames(frames[k], poses[k:k + 1], wl.calib)
-            b = boxes[int(mine[k])]
-            grid.fill_holes(pkg.dilate(b, fill_r), fill_r, pkg.FILL_MEAN, count=False)
-            grid.render_coronal(b, rp, fill_r)
-            le[j][1].record(stream)
-            stream.synchronize()
-            lat_wall.append((time.perf_counter() - w) * 1e3)
-        torch.cuda.synchronize()
-        lat_dev = [a.elapsed_time(b) for a, b in le]
+            return [a.elapsed_time(b) for a, b in le], wall
+
+        nl = min(args.latency_frames, max(n_my - 4, 0))
+        mid = max(0, n_my // 2 - nl // 2)
+        lat_dev, lat_wall = [], []
+        lat_dev_c, lat_wall_c = [], []
+        if nl:
+            frame_latency(3, max(mid - 3, 0), True)  # graph capture + warm-up, untimed
+            lat_dev, lat_wall = frame_latency(nl, mid, True)
+            lat_dev_c, lat_wall_c = frame_latency(nl, mid, False)
 
     stats = grid.stats()
     hbm, peak_src = _peaks()
@@ -456,7 +469,11 @@ def run_ours(args):
         "latency_ms": {"frames": nl, "device_p50": pct(lat_dev, 0.5), "device_p95": pct(lat_dev, 0.95),
                        "device_max": max(lat_dev) if lat_dev else None, "wall_p50": pct(lat_wall, 0.5),
                        "wall_p95": pct(lat_wall, 0.95), "wall_max": max(lat_wall) if lat_wall else None,
-                       "what": "one frame: insert + fill(conservative box+1) + render(box), rank-local"},
+                       "what": "one frame: insert + fill(conservative box+1) + render(box) as one CUDA-graph "
+                               "replay (svr_frame_step), rank-local",
+                       "per_call": {"device_p50": pct(lat_dev_c, 0.5), "device_p95": pct(lat_dev_c, 0.95),
+                                    "wall_p50": pct(lat_wall_c, 0.5),
+                                    "what": "the same kernels launched call by call"}},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
         "gpu_launches": int(launches),

@@ -178,6 +178,15 @@ int svr_fill_holes_boxes(svr_volume* vol, const svr_box* regions, int32_t n, int
  * image).  dirty = NULL re-renders every column of the slab. */
 int svr_render_coronal(svr_volume* vol, const svr_box* dirty, int32_t fill_radius,
                        const svr_render_params* params);
+/* One frame of the incremental pipeline as a single CUDA-graph replay: insert,
+ * r = 1 mean fill of the conservative dirty box (+) 1, depth-band render of its columns.  The graph
+ * is captured on first use (and re-captured when the frame geometry, calibration, render
+ * parameters or a region bound changes); px may be host (pageable or pinned) or device memory.
+ * Asynchronous; dirty_out (may be NULL) receives the conservative box.  Results are identical to
+ * svr_insert_frame + svr_fill_holes + svr_render_coronal over that box. */
+int svr_frame_step(svr_volume* vol, const uint8_t* px, int64_t row_pitch, const svr_rigid* pose,
+                   const svr_calib* calib, int32_t fill_radius, const svr_render_params* params,
+                   svr_box* dirty_out);
 /* svr_render_coronal for a list of dirty regions in one pair of launches. */
 int svr_render_coronal_boxes(svr_volume* vol, const svr_box* dirty, int32_t n, int32_t fill_radius,
                              const svr_render_params* params);

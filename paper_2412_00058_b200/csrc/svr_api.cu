@@ -56,6 +56,29 @@ int svr_fail(int code, const char* fmt, ...) {
                         cudaGetErrorString(e_), __FILE__, __LINE__);                       \
     } while (0)
 
+// Per-frame incremental pipeline (svr_frame_step) captured once as a CUDA graph: frame copy,
+// parameter and region-table uploads from pinned staging, insert, fill of the conservative dirty
+// box (+) r, depth + band render of its columns.  Grid sizes are captured as upper bounds (the
+// kernels retire surplus CTAs), so one graph replays for every frame of a sweep.
+struct FrameGraph {
+    bool ready = false;
+    int w = 0, h = 0, fr = -1;
+    svr_calib cal{};
+    svr_render_params rp{};
+    long long fill_ctas = 0, depth_ctas = 0, band_ctas = 0;
+    uint8_t* d_frame = nullptr;
+    uint8_t* h_frame = nullptr;      // pinned staging for pageable / pitched host frames
+    FrameParams* h_fp = nullptr;     // pinned
+    FrameParams* d_fp = nullptr;
+    unsigned char* h_tiles = nullptr;  // pinned: BoxTiles | ColTiles depth | ColTiles band
+    unsigned char* d_tiles = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t frame_copy = nullptr;
+    cudaEvent_t done = nullptr;
+    int kernels = 0;
+};
+
 struct svr_volume {
     svr_grid_desc d{};
     int device = 0;
@@ -97,12 +120,14 @@ struct svr_volume {
     uint64_t launches = 0;
     uint64_t frames = 0;
     ull* d_work = nullptr;          // deferred exact-path chunks of k_pnn_plane
+    FrameGraph fg;                  // svr_frame_step graph
     void* d_tiles = nullptr;        // region tables of the multi-box fill / render launches
     size_t tiles_cap = 0;
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
     int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 step counters, 0 carries
+    int depth_seg = 4;          // SVR_DEPTH_SEG: threads per column in k_depth (4, or 1)
     int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
     int plane_tw_cur = 4;       // the width chosen for the current insert call
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
@@ -620,6 +645,15 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFree(v->d_work);
     cudaFree(v->d_tiles);
     cudaFree(v->d_work_n);
+    if (v->fg.exec) cudaGraphExecDestroy(v->fg.exec);
+    if (v->fg.graph) cudaGraphDestroy(v->fg.graph);
+    if (v->fg.done) cudaEventDestroy(v->fg.done);
+    cudaFree(v->fg.d_frame);
+    cudaFree(v->fg.d_fp);
+    cudaFree(v->fg.d_tiles);
+    cudaFreeHost(v->fg.h_frame);
+    cudaFreeHost(v->fg.h_fp);
+    cudaFreeHost(v->fg.h_tiles);
     for (int i = 0; i < 2; ++i) {
         cudaFree(v->d_stage[i]);
         cudaFreeHost(v->h_stage[i]);
@@ -657,6 +691,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         v->fill_ty = (t == 4 || t == 12 || t == 16) ? t : 8;
     }
     if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("SVR_DEPTH_SEG")) v->depth_seg = std::atoi(e) == 4 ? 4 : 1;
     if (const char* e = std::getenv("SVR_PLANE_TW")) v->plane_tw = std::atoi(e) == 6 ? 6 : 4;
     if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
@@ -1429,10 +1464,10 @@ static bool render_regions(const svr_volume* v, const svr_box* dirty, int fr, in
     return true;
 }
 
-static long long tile_cols(std::vector<ColTiles>& ct) {
+static long long tile_cols(std::vector<ColTiles>& ct, int cols_per_cta = 128) {
     long long total = 0;
     for (ColTiles& t : ct) {
-        t.ntx = (t.x1 - t.x0 + 1 + 127) / 128;
+        t.ntx = (t.x1 - t.x0 + cols_per_cta) / cols_per_cta;
         t.first = total;
         total += (long long)t.ntx * (t.z1 - t.z0 + 1);
     }
@@ -1457,7 +1492,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
         }
     }
     if (dt.empty()) return SVR_OK;
-    const long long nd = tile_cols(dt), nm = tile_cols(mt);
+    const long long nd = tile_cols(dt, 128 / v->depth_seg), nm = tile_cols(mt);
     // one upload holds both tables: [dt | mt]
     std::vector<ColTiles> both(dt);
     both.insert(both.end(), mt.begin(), mt.end());
@@ -1466,8 +1501,12 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
     const ColTiles* ddt = (const ColTiles*)d;
     const ColTiles* dmt = ddt + dt.size();
     const GridDev g = dev_grid(v->d);
-    k_depth<<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
-                                                 p->fill_mode, v->r_depth);
+    if (v->depth_seg == 4)
+        k_depth<4><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
+                                                        p->fill_mode, v->r_depth);
+    else
+        k_depth<1><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
+                                                        p->fill_mode, v->r_depth);
     v->launches++;
     CKL();
     k_band<<<grid_1d(nm), 128, 0, v->stream>>>(v->acc, v->fill, g, dmt, (int)mt.size(), p->median_radius,
@@ -1733,5 +1772,160 @@ extern "C" int svr_synth_frames(void* dst, int32_t w, int32_t h, int32_t first, 
     CKL();
     CK(cudaFreeAsync(dp, s));
     CK(cudaStreamSynchronize(s));
+    return SVR_OK;
+}
+
+
+// ---------------------------------------------------------------- per-frame graph
+static constexpr size_t kFgTileBytes = sizeof(BoxTiles) + 2 * sizeof(ColTiles);
+
+static bool fg_matches(const FrameGraph& f, int w, int h, int fr, const svr_calib& c,
+                       const svr_render_params& p, long long nf, long long nd, long long nb) {
+    return f.ready && f.w == w && f.h == h && f.fr == fr && !std::memcmp(&f.cal, &c, sizeof c) &&
+           !std::memcmp(&f.rp, &p, sizeof p) && nf <= f.fill_ctas && nd <= f.depth_ctas && nb <= f.band_ctas;
+}
+
+static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, const svr_render_params& p,
+                      long long nf, long long nd, long long nb) {
+    FrameGraph& f = v->fg;
+    CK(cudaStreamSynchronize(v->stream));
+    if (f.exec) cudaGraphExecDestroy(f.exec);
+    if (f.graph) cudaGraphDestroy(f.graph);
+    f.exec = nullptr;
+    f.graph = nullptr;
+    f.ready = false;
+    if (f.w != w || f.h != h || !f.d_frame) {
+        cudaFree(f.d_frame);
+        cudaFreeHost(f.h_frame);
+        f.d_frame = nullptr;
+        f.h_frame = nullptr;
+        CK(cudaMalloc(&f.d_frame, (size_t)w * h));
+        CK(cudaMallocHost(&f.h_frame, (size_t)w * h));
+    }
+    if (!f.d_fp) {
+        CK(cudaMalloc(&f.d_fp, sizeof(FrameParams)));
+        CK(cudaMallocHost(&f.h_fp, sizeof(FrameParams)));
+        CK(cudaMalloc(&f.d_tiles, kFgTileBytes));
+        CK(cudaMallocHost(&f.h_tiles, kFgTileBytes));
+        CK(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
+    }
+    if (!v->d_work) {
+        v->work_cap = 1u << 20;
+        CK(cudaMalloc(&v->d_work, sizeof(ull) * v->work_cap));
+        CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
+    }
+    if (int e = ensure_fan(v, c)) return e;
+    // bounds with headroom: later frames of a sweep rarely need a larger graph
+    f.fill_ctas = std::max(f.fill_ctas, nf + nf / 4 + 1);
+    f.depth_ctas = std::max(f.depth_ctas, nd + nd / 4 + 1);
+    f.band_ctas = std::max(f.band_ctas, nb + nb / 4 + 1);
+    int ylo, yhi, above, below;
+    render_ints(&p, v->d.voxel_mm, v->d.ny, &ylo, &yhi, &above, &below);
+    const GridDev g = dev_grid(v->d);
+    const DevCalib dc = dev_calib(c);
+    const long long l0 = v->launches;
+    CK(cudaStreamBeginCapture(v->stream, cudaStreamCaptureModeThreadLocal));
+    cudaMemcpyAsync(f.d_frame, f.h_frame, (size_t)w * h, cudaMemcpyDefault, v->stream);
+    cudaMemcpyAsync(f.d_fp, f.h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, v->stream);
+    cudaMemcpyAsync(f.d_tiles, f.h_tiles, kFgTileBytes, cudaMemcpyHostToDevice, v->stream);
+    int e = insert_device(v, kModeInsert, f.d_frame, w, (long long)w * h, w, h, 1, f.d_fp, dc, false, false,
+                          nullptr, nullptr, 0, v->d_stats);
+    const BoxTiles* bt = (const BoxTiles*)f.d_tiles;
+    const ColTiles* dt = (const ColTiles*)(f.d_tiles + sizeof(BoxTiles));
+    const ColTiles* mt = dt + 1;
+    if (!e) {
+        // 4-plane marches: a single frame's box is shallow in z, short marches cut its latency
+        k_fill_warp<4, 1, 8><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, v->d_counter);
+        k_depth<4><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, dt, 1, ylo, yhi,
+                                                                  p.fill_mode, v->r_depth);
+        k_band<<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, mt, 1, p.median_radius, above,
+                                                             below, p.fill_mode, v->r_depth, v->r_mdepth,
+                                                             v->r_mean, v->r_max);
+    }
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(v->stream, &graph);
+    if (e) {
+        if (graph) cudaGraphDestroy(graph);
+        return e;
+    }
+    CK(ce);
+    f.graph = graph;
+    f.kernels = (int)(v->launches - l0) + 3;
+    v->launches = l0;
+    CK(cudaGraphInstantiate(&f.exec, f.graph, 0));
+    // the frame copy is the graph's memcpy node writing d_frame: its source is set per call
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(f.graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(f.graph, nodes.data(), &nn));
+    f.frame_copy = nullptr;
+    for (cudaGraphNode_t n : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(n, &t));
+        if (t != cudaGraphNodeTypeMemcpy) continue;
+        cudaMemcpy3DParms mp;
+        CK(cudaGraphMemcpyNodeGetParams(n, &mp));
+        if (mp.dstPtr.ptr == f.d_frame) f.frame_copy = n;
+    }
+    if (!f.frame_copy) return fail(SVR_E_CUDA, "frame graph: frame copy node not found");
+    f.w = w;
+    f.h = h;
+    f.fr = fr;
+    f.cal = c;
+    f.rp = p;
+    f.ready = true;
+    return SVR_OK;
+}
+
+extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, const svr_rigid* pose,
+                              const svr_calib* c, int32_t fill_radius, const svr_render_params* p,
+                              svr_box* dirty_out) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "frame step needs a PNN volume");
+    if (!px || !pose || !p) return fail(SVR_E_INVALID, "NULL argument");
+    if (int e = check_calib(c, c ? c->crop_w : 0, c ? c->crop_h : 0)) return e;
+    const int w = c->crop_w, h = c->crop_h;
+    if (pitch < w) return fail(SVR_E_INVALID, "row pitch %lld < width %d", (long long)pitch, w);
+    if (fill_radius != 1) return fail(SVR_E_INVALID, "the frame graph runs the r = 1 mean fill");
+    if (p->median_radius < 0 || p->median_radius > 2) return fail(SVR_E_INVALID, "median_radius must be 0..2");
+    FrameGraph& f = v->fg;
+    if (f.done) CK(cudaEventSynchronize(f.done));  // staging of the previous frame consumed
+    const svr_box b = frame_box(v->d, *c, *pose);
+    Box fb;
+    svr_box bd{b.x0 - 1, b.y0 - 1, b.z0 - 1, b.x1 + 1, b.y1 + 1, b.z1 + 1};
+    ColTiles ct[2];
+    const bool any = b.x0 <= b.x1 && clip_box(v, &bd, &fb) &&
+                     render_regions(v, &b, fill_radius, p->median_radius, &ct[0], &ct[1]);
+    if (!any) {  // frame entirely outside the slab: a plain insert counts its pixels
+        if (dirty_out) *dirty_out = svr_box{1, 1, 1, 0, 0, 0};
+        return svr_insert_frames(v, px, pitch, pitch * h, w, h, 1, pose, c, 0, nullptr, nullptr);
+    }
+    BoxTiles bt;
+    bt.b = fb;
+    bt.ntx = (fb.x1 - fb.x0 + 1 + 119) / 120;
+    bt.nty = (fb.y1 - fb.y0 + 1 + 7) / 8;
+    bt.first = 0;
+    const long long nf = (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 3) / 4);
+    std::vector<ColTiles> cv{ct[0]}, mv{ct[1]};
+    const long long nd = tile_cols(cv, 32), nm = tile_cols(mv);
+    if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm))
+        if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;
+    if (int e = make_params(*pose, prep_ctx(*c, v->d), c->scale_x_mm, c->scale_y_mm, f.h_fp)) return e;
+    std::memcpy(f.h_tiles, &bt, sizeof bt);
+    std::memcpy(f.h_tiles + sizeof(BoxTiles), &cv[0], sizeof(ColTiles));
+    std::memcpy(f.h_tiles + sizeof(BoxTiles) + sizeof(ColTiles), &mv[0], sizeof(ColTiles));
+    // frame source: device / pinned packed frames are copied straight from the caller
+    bool pinned = false;
+    const void* src = px;
+    if (!(is_device_ptr(px, &pinned) || pinned) || pitch != w) {
+        for (int r = 0; r < h; ++r) std::memcpy(f.h_frame + (size_t)r * w, px + (size_t)r * pitch, (size_t)w);
+        src = f.h_frame;
+    }
+    CK(cudaGraphExecMemcpyNodeSetParams1D(f.exec, f.frame_copy, f.d_frame, src, (size_t)w * h, cudaMemcpyDefault));
+    CK(cudaGraphLaunch(f.exec, v->stream));
+    CK(cudaEventRecord(f.done, v->stream));
+    v->frames += 1;
+    v->launches += f.kernels;
+    if (dirty_out) *dirty_out = b;
     return SVR_OK;
 }

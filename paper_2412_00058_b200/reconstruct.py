@@ -137,6 +137,21 @@ class VoxelGrid:
                                       C.byref(calib), int(skip_zero), None, None))
         return None
 
+    def frame_step(self, frame, pose, calib: Calib, fill_radius: int = 1,
+                   params: RenderParams = None) -> Box:
+        """One incremental frame (insert -> fill(box (+) 1) -> render(box)) as a CUDA-graph
+        replay (svr_frame_step); asynchronous, returns the conservative dirty box."""
+        from .synth import render_params
+        keep, p, pitch, _, n, h, w = _frames_view(frame)
+        if n != 1:
+            raise InvalidInput("frame_step takes one frame")
+        pa = rigid_array(pose)
+        b = Box()
+        check(lib().svr_frame_step(self._h, p, pitch, rigid_ptr(pa), C.byref(calib), int(fill_radius),
+                                   C.byref(params or render_params()), C.byref(b)))
+        self._keep = keep
+        return b
+
     def fill_holes(self, region=None, radius: int = 1, mode: int = _abi.FILL_MEAN,
                    count: bool = True) -> Optional[int]:
         """fill_holes over exactly `region` (None = whole slab)."""

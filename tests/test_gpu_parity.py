@@ -38,7 +38,9 @@ def test_cfg1_batch_bitexact():
     assert st["frames_inserted"] == wl.nframes
 
 
-def test_cfg1_fill_and_render_bitexact():
+@pytest.mark.parametrize("depth_seg", ["4", "1"])
+def test_cfg1_fill_and_render_bitexact(depth_seg, monkeypatch):
+    monkeypatch.setenv("SVR_DEPTH_SEG", depth_seg)  # k_depth: 4 threads per column, or 1
     wl = synth.cfg1()
     frames = wl.frames_np()
     grid = _grid(wl)
@@ -405,3 +407,34 @@ def test_slab_sharded_bench_step_equals_unsharded(world):
         assert np.array_equal(m, mean_f[o0:o1]) and np.array_equal(x, max_f[o0:o1])
         assert np.array_equal(d, dep_f[o0:o1])
         del g
+
+
+@pytest.mark.parametrize("source", ["host", "device", "pinned"])
+def test_frame_step_graph_equals_per_call_pipeline(source):
+    """svr_frame_step (one CUDA-graph replay per frame) against the per-call pipeline
+    insert -> fill(box (+) 1) -> render(box): accumulators, fill layer and coronal images equal,
+    including frames whose box is clipped by the grid and one wholly outside it."""
+    import torch
+    wl = synth.cfg1(nframes=40)
+    frames = wl.frames_np()
+    poses = wl.poses.copy()
+    poses[5]["tx"] += 1000.0  # outside the grid: the early plain-insert path
+    rp = synth.render_params(depth_lo_mm=5.0, depth_hi_mm=40.0)
+    a, b = _grid(wl), _grid(wl)
+    dev = torch.from_numpy(frames).cuda()
+    pin = torch.from_numpy(frames).pin_memory()
+    for k in range(wl.nframes):
+        src = {"host": frames[k], "device": dev[k], "pinned": pin[k]}[source]
+        box = a.frame_step(src, poses[k:k + 1], wl.calib, 1, rp)
+        b.insert_frames(frames[k], poses[k:k + 1], wl.calib)
+        if not box.empty():
+            b.fill_holes(pkg.dilate(box, 1), 1, pkg.FILL_MEAN, count=False)
+            b.render_coronal(box, rp, 1)
+    a.sync()
+    sa, ca = a.accumulators()
+    sb, cb = b.accumulators()
+    assert np.array_equal(ca, cb) and np.array_equal(sa, sb)
+    assert np.array_equal(a.fill_layer(), b.fill_layer())
+    for x, y in zip(a.read_coronal(), b.read_coronal()):
+        assert np.array_equal(x, y)
+    assert a.stats()["frames_inserted"] == wl.nframes
