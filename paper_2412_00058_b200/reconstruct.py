@@ -292,8 +292,14 @@ def run_incremental(frames: Iterable, poses, calib: Calib, grid: VoxelGrid, hole
     percentiles (percentile as core.hpp:101-107)."""
     pa = rigid_array(poses)
     lat = []
+    graph = render is not None and hole_radius == 1 and fill_mode == _abi.FILL_MEAN and not skip_zero
     for k, fr in enumerate(frames):
         t0 = time.perf_counter()
+        if graph:  # the whole per-frame step as one CUDA-graph replay (svr_frame_step)
+            grid.frame_step(fr, pa[k:k + 1], calib, 1, render)
+            grid.sync()
+            lat.append((time.perf_counter() - t0) * 1e3)
+            continue
         grid.insert_frames(fr, pa[k:k + 1], calib, skip_zero)
         b = frame_bounds(grid.desc, calib, pa[k:k + 1])
         if not b.empty():
