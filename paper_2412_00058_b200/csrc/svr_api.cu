@@ -132,7 +132,7 @@ struct svr_volume {
     int plane_tw_cur = 4;       // the width chosen for the current insert call
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
-    int fill_zc = 16;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
+    int fill_zc = 32;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
     int fill_mode = SVR_FILL_MEAN;  // mode of the latest fill_holes: decodes the fill layer on readout
     bool fill_tma = false;      // SVR_FILL_KERNEL=tma selects k_fill_tma (opt-in: 0.43 vs 0.385 ms)
     int fill_tma_zc = 32;       // SVR_FILL_TMA_ZC: planes per CTA in k_fill_tma (16/32)
