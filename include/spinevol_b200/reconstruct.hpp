@@ -185,6 +185,23 @@ public:
         check(svr_get_stats(h_, &s));
         return s;
     }
+    // one incremental frame (insert -> mean fill of box (+) 1 -> render) as a CUDA-graph replay
+    DirtyRegion frame_step(const uint8_t* px, int64_t row_pitch, const svr_rigid& pose,
+                           const svr_calib& calib, const svr_render_params& p, int fill_radius = 1) {
+        DirtyRegion r;
+        check(svr_frame_step(h_, px, row_pitch, &pose, &calib, fill_radius, &p, &r.b));
+        return r;
+    }
+    // volume file: raw u8 values, x fastest
+    void export_volume(const std::string& path, bool apply_fills = true) {
+        check(svr_export_volume(h_, path.c_str(), apply_fills ? 1 : 0));
+    }
+    // export_slices along x: returns the file count
+    int export_slices(const std::string& dir, bool apply_fills = true, int digits = 4) {
+        int32_t n = 0;
+        check(svr_export_slices(h_, dir.c_str(), apply_fills ? 1 : 0, digits, &n));
+        return n;
+    }
     DirtyRegion frame_bounds(const svr_calib& calib, const svr_rigid& pose) const {
         DirtyRegion r;
         check(svr_frame_bounds(&desc_, &calib, &pose, &r.b));
@@ -224,8 +241,15 @@ inline IncrementalStats run_incremental(VoxelGrid& g, const uint8_t* frames, int
                                         bool skip_zero = false) {
     std::vector<double> lat;
     lat.reserve((size_t)n);
+    const bool graph = render && hole_radius == 1 && fill_mode == SVR_FILL_MEAN && !skip_zero;
     for (int k = 0; k < n; ++k) {
         const auto t0 = std::chrono::steady_clock::now();
+        if (graph) {  // the per-frame step as one CUDA-graph replay
+            g.frame_step(frames + (size_t)k * w * h, w, poses[k], calib, *render, 1);
+            g.sync();
+            lat.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+            continue;
+        }
         check(svr_insert_frames(g.handle(), frames + (size_t)k * w * h, w, (int64_t)w * h, w, h, 1,
                                 poses + k, &calib, skip_zero ? 1 : 0, nullptr, nullptr));
         const DirtyRegion b = g.frame_bounds(calib, poses[k]);
@@ -254,8 +278,50 @@ inline IncrementalStats run_incremental(VoxelGrid& g, const uint8_t* frames, int
     return st;
 }
 
+// ---- binary PGM (image.hpp:34-72) through the native reader/writer
+struct Image {
+    int width = 0, height = 0;
+    std::vector<uint8_t> data;  // row-major
+};
+
+inline Image read_pgm(const std::string& path) {
+    Image img;
+    int32_t w = 0, h = 0;
+    check(svr_pgm_info(path.c_str(), &w, &h));
+    img.width = w;
+    img.height = h;
+    img.data.resize((size_t)w * h);
+    check(svr_pgm_read(path.c_str(), img.data.data(), std::max(w, 1), w, h));
+    return img;
+}
+
+inline void write_pgm(const uint8_t* px, int w, int h, const std::string& path) {
+    check(svr_pgm_write(path.c_str(), px, std::max(w, 1), w, h));
+}
+
+// ---- segmentation host halves (SPEC.md segment module)
+inline double cut_depth_alg1(double p_c1, double p_cn, double K, double D, double L, double axial_extent_mm) {
+    double c = 0;
+    check(svr_cut_depth_alg1(p_c1, p_cn, K, D, L, axial_extent_mm, &c));
+    return c;
+}
+
+inline std::vector<double> smooth_depths(const std::vector<double>& depths, const std::vector<uint8_t>& valid,
+                                         int window = 11) {
+    if (depths.size() != valid.size()) throw InvalidInput("depths / valid size mismatch");
+    std::vector<double> out(depths.size());
+    check(svr_smooth_depths(depths.data(), valid.data(), (int32_t)depths.size(), window, out.data()));
+    return out;
+}
+
 #ifdef SPINEVOL_B200_REFERENCE_TYPES
 // ---- drop-in overloads on the reference's own value types (geometry.hpp, image.hpp)
+inline spinevol::Image8 read_pgm_image8(const std::string& path) {
+    Image i = read_pgm(path);
+    spinevol::Image8 img(i.width, i.height);
+    img.data = std::move(i.data);
+    return img;
+}
 inline svr_rigid to_svr(const spinevol::RigidTransform& t) {
     return svr_rigid{t.rotation.w, t.rotation.x, t.rotation.y, t.rotation.z,
                      t.translation.x, t.translation.y, t.translation.z};

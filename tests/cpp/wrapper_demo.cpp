@@ -9,6 +9,7 @@
 #include <cstring>
 #include <fstream>
 #include <iostream>
+#include <string>
 #include <vector>
 
 #include "spinevol_b200/reconstruct.hpp"
@@ -48,6 +49,29 @@ static int host_checks() {
     spinevol::Vec3 ref = spinevol::pixel_to_world(100, 200, rc, spinevol::RigidTransform::identity());
     if (!(w[0] == ref.x && w[1] == ref.y && w[2] == ref.z)) return 4;
 #endif
+    // PGM round trip and the segmentation host halves (no GPU needed)
+    {
+        std::vector<uint8_t> img(37 * 21);
+        for (size_t i = 0; i < img.size(); ++i) img[i] = (uint8_t)(i * 7);
+        const std::string path = "/tmp/svr_wrapper_demo.pgm";
+        sb::write_pgm(img.data(), 37, 21, path);
+        sb::Image back = sb::read_pgm(path);
+        if (back.width != 37 || back.height != 21 || back.data != img) return 5;
+#ifdef SPINEVOL_B200_REFERENCE_TYPES
+        spinevol::Image8 ri = spinevol::read_pgm(path);  // the reference's own reader agrees
+        if (ri.data != img) return 6;
+#endif
+        if (sb::cut_depth_alg1(100.0, 100.0, 0.04, 35.0, 500.0, 60.0) != 45.0) return 7;
+        std::vector<double> d{35, 35, 80, 35, 35};
+        std::vector<uint8_t> v(5, 1);
+        for (double x : sb::smooth_depths(d, v, 5))
+            if (x != 35.0) return 8;
+        try {
+            sb::read_pgm("/nonexistent/x.pgm");
+            return 9;
+        } catch (const sb::IoError&) {
+        }
+    }
     std::puts("host ok");
     return 0;
 }
