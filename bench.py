@@ -361,7 +361,9 @@ def run_ours(args):
             grid.fill_holes_boxes(fill_boxes, fill_r, pkg.FILL_MEAN, count=False)
             grid.render_coronal_boxes(render_boxes, rp, fill_r)
             gather()
-            grid.read_coronal_into(own[0], own[1] - 1, mean_h, max_h)
+            # the step's result read back into pinned host buffers, enqueued behind the render so
+            # the next step's H2D staging overlaps this step's fill / render / read-back
+            grid.read_coronal_into(own[0], own[1] - 1, mean_h, max_h, wait=False)
 
         e2e_step()
         torch.cuda.synchronize()

@@ -193,6 +193,10 @@ int svr_render_coronal_boxes(svr_volume* vol, const svr_box* dirty, int32_t n, i
 /* Copy rendered rows z in [z0,z1] (global, inside the slab) as nx-wide row-major images. */
 int svr_read_coronal(svr_volume* vol, int32_t z0, int32_t z1, float* mean_out, float* max_out,
                      int32_t* depth_out);
+/* svr_read_coronal enqueued on the handle's stream without waiting (outputs pinned or device;
+ * complete after svr_sync or the stream's next synchronisation). */
+int svr_read_coronal_async(svr_volume* vol, int32_t z0, int32_t z1, float* mean_out, float* max_out,
+                           int32_t* depth_out);
 
 /* coronal_projection: u8 max / mean over non-empty voxels along depth_axis
  * (0=x,1=y,2=z); use_fills also admits filled voxels.  Output is row-major over the two

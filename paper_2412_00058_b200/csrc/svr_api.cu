@@ -1530,8 +1530,21 @@ extern "C" int svr_render_coronal_boxes(svr_volume* v, const svr_box* dirty, int
     return render_boxes(v, dirty, n, fill_radius, p);
 }
 
+static int read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv, int32_t* depth,
+                        bool sync);
+
 extern "C" int svr_read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv,
                                 int32_t* depth) {
+    return read_coronal(v, z0, z1, mean, maxv, depth, true);
+}
+
+extern "C" int svr_read_coronal_async(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv,
+                                      int32_t* depth) {
+    return read_coronal(v, z0, z1, mean, maxv, depth, false);
+}
+
+static int read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv, int32_t* depth,
+                        bool sync) {
     VOL_CHECK(v);
     if (!v->acc) return fail(SVR_E_INVALID, "render needs a PNN volume");
     if (z0 < v->d.z_begin || z1 >= v->d.z_end || z0 > z1)
@@ -1540,7 +1553,7 @@ extern "C" int svr_read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* me
     if (mean) CK(cudaMemcpyAsync(mean, v->r_mean + off, cnt * sizeof(float), cudaMemcpyDefault, v->stream));
     if (maxv) CK(cudaMemcpyAsync(maxv, v->r_max + off, cnt * sizeof(float), cudaMemcpyDefault, v->stream));
     if (depth) CK(cudaMemcpyAsync(depth, v->r_mdepth + off, cnt * sizeof(int), cudaMemcpyDefault, v->stream));
-    CK(cudaStreamSynchronize(v->stream));
+    if (sync) CK(cudaStreamSynchronize(v->stream));
     return SVR_OK;
 }
 

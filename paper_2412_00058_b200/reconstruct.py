@@ -193,9 +193,11 @@ class VoxelGrid:
         shp = (z1 - z0 + 1, self.desc.nx)
         return mean.reshape(shp), mx.reshape(shp), dep.reshape(shp)
 
-    def read_coronal_into(self, z0, z1, mean, mx, depth=None):
-        """Copy rendered rows into caller buffers (host or device, e.g. torch tensors)."""
-        check(lib().svr_read_coronal(self._h, z0, z1, ptr(mean), ptr(mx), ptr(depth)))
+    def read_coronal_into(self, z0, z1, mean, mx, depth=None, wait: bool = True):
+        """Copy rendered rows into caller buffers (host or device, e.g. torch tensors).
+        wait=False only enqueues the copy on the grid's stream (pinned / device outputs)."""
+        fn = lib().svr_read_coronal if wait else lib().svr_read_coronal_async
+        check(fn(self._h, z0, z1, ptr(mean), ptr(mx), ptr(depth)))
 
     def coronal_projection(self, mode: int = _abi.PROJ_MAX, depth_axis: int = 2,
                            use_fills: bool = False) -> np.ndarray:
