@@ -443,14 +443,25 @@ def run_ours(args):
         s = sorted(v)
         return s[int(p * (len(s) - 1) + 0.5)] if s else None
 
-    traffic = None
+    traffic, atomics = None, None
     tf = os.path.join(ROOT, "profiles", "insert_traffic.json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                nc = json.load(f)
+            traffic = nc.get("dram_bytes_per_launch")
+            # atomic throughput of K1 (north_star): ncu counts per launch over the live launch time
+            if nc.get("l2_red_requests_per_launch"):
+                atomics = {
+                    "source": "ncu counts per launch (profiles/insert_traffic.json) / live K1 time",
+                    "l2_red_requests_per_s": nc["l2_red_requests_per_launch"] / ins_s,
+                    "l2_red_sectors_per_s": nc["l2_red_sectors_per_launch"] / ins_s,
+                    "l2_red_sector_hit_rate": nc.get("l2_red_sector_hit_rate"),
+                    "smem_atom_wavefronts_per_s": nc["smem_atom_wavefronts_per_launch"] / ins_s,
+                    "smem_atom_per_pixel": 1.0,
+                }
         except Exception:
-            traffic = None
+            traffic, atomics = None, None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -467,7 +478,8 @@ def run_ours(args):
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_model": "sum_f (W*H + 12*U_f), U_f distinct voxels of frame f (mean %.0f)"
-                                    % float(U.mean())},
+                                    % float(U.mean()),
+                     "atomics": atomics},
         "latency_ms": {"frames": nl, "device_p50": pct(lat_dev, 0.5), "device_p95": pct(lat_dev, 0.95),
                        "device_max": max(lat_dev) if lat_dev else None, "wall_p50": pct(lat_wall, 0.5),
                        "wall_p95": pct(lat_wall, 0.95), "wall_max": max(lat_wall) if lat_wall else None,

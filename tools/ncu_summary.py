@@ -31,6 +31,10 @@ KEYS = {
     "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio": "stall_barrier",
     "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio": "stall_math_throttle",
     "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio": "stall_lg_throttle",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum": "smem_atom_wavefronts",
+    "lts__t_requests_srcunit_tex_op_red.sum": "l2_red_requests",
+    "lts__t_sectors_srcunit_tex_op_red.sum": "l2_red_sectors",
+    "lts__t_sectors_srcunit_tex_op_red_lookup_hit.sum": "l2_red_sectors_hit",
 }
 
 
@@ -71,6 +75,11 @@ def main():
         d = ks[0]
         with open(a.traffic, "w") as f:
             json.dump({"kernel": d["kernel"], "dram_bytes_per_launch": d["dram_read"] + d["dram_write"],
+                       "smem_atom_wavefronts_per_launch": d.get("smem_atom_wavefronts"),
+                       "l2_red_requests_per_launch": d.get("l2_red_requests"),
+                       "l2_red_sectors_per_launch": d.get("l2_red_sectors"),
+                       "l2_red_sector_hit_rate": (d["l2_red_sectors_hit"] / d["l2_red_sectors"])
+                       if d.get("l2_red_sectors") else None,
                        "source": f"{a.out} (ncu --set full, cfg2 batch of 2400 frames, one launch)"},
                       f, indent=1)
     print(f"{len(ds)} launches summarised")
