@@ -438,3 +438,45 @@ def test_frame_step_graph_equals_per_call_pipeline(source):
     for x, y in zip(a.read_coronal(), b.read_coronal()):
         assert np.array_equal(x, y)
     assert a.stats()["frames_inserted"] == wl.nframes
+
+
+def test_edge_cases():
+    """Empty and degenerate inputs: zero frames, a frame wholly outside the grid (all pixels
+    counted OOB, empty dirty box), an empty fill region, a render over an empty box, a pitched
+    host frame through the frame graph, and readouts of a z-slab volume."""
+    import torch
+    wl = synth.small_linear(nframes=6)
+    frames = wl.frames_np()
+    g = _grid(wl)
+    g.insert_frames(frames[:0], wl.poses[:0], wl.calib)  # no-op
+    assert g.stats()["frames_inserted"] == 0
+    far = wl.poses[:1].copy()
+    far["tz"] += 1e4
+    boxes, u = g.insert_frames(frames[:1], far, wl.calib, want_boxes=True)
+    st = g.stats()
+    assert u.empty() and boxes[0].empty()
+    assert st["pixels_oob"] == wl.w * wl.h and st["pixels_inserted"] == 0
+    assert g.fill_holes((5, 5, 5, 4, 4, 4), 1, pkg.FILL_MEAN) == 0
+    g.render_coronal((1, 1, 1, 0, 0, 0), synth.render_params(), 1)
+    # pitched host frame (row pitch 80 > width 64) through svr_frame_step == per-call pipeline
+    pitched = np.zeros((wl.h, 80), np.uint8)
+    pitched[:, :wl.w] = frames[2]
+    rp = synth.render_params(depth_lo_mm=1.0, depth_hi_mm=12.0)
+    a, b = _grid(wl), _grid(wl)
+    box = a.frame_step(pitched[:, :wl.w], wl.poses[2:3], wl.calib, 1, rp)
+    b.insert_frames(frames[2], wl.poses[2:3], wl.calib)
+    b.fill_holes(pkg.dilate(box, 1), 1, pkg.FILL_MEAN)
+    b.render_coronal(box, rp, 1)
+    a.sync()
+    for x, y in zip(a.accumulators(), b.accumulators()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.fill_layer(), b.fill_layer())
+    # a z-slab volume reads back exactly its planes
+    full = _grid(wl)
+    full.insert_frames(frames, wl.poses, wl.calib)
+    slab = _grid(wl, z_range=(10, 30))
+    slab.insert_frames(frames, wl.poses, wl.calib)
+    s_full, c_full = full.accumulators()
+    s_sl, c_sl = slab.accumulators()
+    assert np.array_equal(c_sl, c_full[10:30]) and np.array_equal(s_sl, s_full[10:30])
+    assert np.array_equal(slab.values(), full.values()[10:30])
