@@ -231,6 +231,10 @@ int svr_count_footprint(svr_volume* vol, const uint8_t* px, int64_t row_pitch,
                         const svr_rigid* poses, const svr_calib* calib, int32_t skip_zero,
                         int64_t* distinct_out);
 
+/* Self-test of the device VoxelGrid::value rounding: checks every count in [1, 255] and every
+ * reachable sum against integer division; writes the mismatch count (0 expected). */
+int svr_selftest_value_rounding(int device, int64_t* mismatches);
+
 /* Synthetic B-scan generator (bench input, BASELINE configs): writes nframes frames of
  * w x h u8 into device memory `dst` (row pitch w).  kind 0 = linear speckle + bone arcs,
  * 1 = log-compressed fan speckle + bright band.  Deterministic in (seed, frame). */

@@ -119,6 +119,7 @@ SIGNATURES = {
     "svr_get_stats": (C.c_int, [P, PS]),
     "svr_count_footprint": (C.c_int, [P, P, I64, I64, I32, I32, I32, PR, PC, I32, C.POINTER(I64)]),
     "svr_synth_frames": (C.c_int, [P, I32, I32, I32, I32, PC, PR, I32, U64, C.c_int, P]),
+    "svr_selftest_value_rounding": (C.c_int, [C.c_int, C.POINTER(I64)]),
     "svr_export_slices_x": (C.c_int, [P, I32, P]),
     "svr_export_slices": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(I32)]),
     "svr_export_volume": (C.c_int, [P, C.c_char_p, I32]),

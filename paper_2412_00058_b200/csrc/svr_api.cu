@@ -1942,3 +1942,18 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     if (dirty_out) *dirty_out = b;
     return SVR_OK;
 }
+
+extern "C" int svr_selftest_value_rounding(int device, int64_t* mismatches) {
+    if (!mismatches) return fail(SVR_E_INVALID, "mismatches is NULL");
+    CK(cudaSetDevice(device));
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(unsigned long long)));
+    CK(cudaMemset(d, 0, sizeof(unsigned long long)));
+    k_selftest_value<<<255, 256>>>(d);
+    CKL();
+    unsigned long long h = 0;
+    CK(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *mismatches = (int64_t)h;
+    return SVR_OK;
+}

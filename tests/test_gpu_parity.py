@@ -480,3 +480,13 @@ def test_edge_cases():
     s_sl, c_sl = slab.accumulators()
     assert np.array_equal(c_sl, c_full[10:30]) and np.array_equal(s_sl, s_full[10:30])
     assert np.array_equal(slab.values(), full.values()[10:30])
+
+
+def test_value_rounding_selftest():
+    """Device acc_value (round(sum / count) via an approximate divide + 1/2 offset) equals
+    integer division for every count in [1, 255] and every reachable sum."""
+    import ctypes as C
+    from paper_2412_00058_b200 import _abi
+    bad = C.c_int64(-1)
+    _abi.check(_abi.lib().svr_selftest_value_rounding(0, C.byref(bad)))
+    assert bad.value == 0
