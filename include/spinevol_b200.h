@@ -190,6 +190,13 @@ int svr_frame_step(svr_volume* vol, const uint8_t* px, int64_t row_pitch, const 
 /* svr_render_coronal for a list of dirty regions in one pair of launches. */
 int svr_render_coronal_boxes(svr_volume* vol, const svr_box* dirty, int32_t n, int32_t fill_radius,
                              const svr_render_params* params);
+/* Fused render + gather (multi-GPU): every later render also stores the mean / max of the owned
+ * rows [own_z0, own_z1) straight into each of the n images (device pointers, typically the
+ * ranks' symmetric-memory peers over NVLink; each a [2][nz][nx] f32 image: mean plane then max
+ * plane, global z), so no all-gather has to follow.  n = 0 switches it off.  The caller orders
+ * the ranks (e.g. a symmetric-memory barrier) before reading. */
+int svr_set_gather_targets(svr_volume* vol, void* const* images, int32_t n, int32_t own_z0,
+                           int32_t own_z1);
 /* Copy rendered rows z in [z0,z1] (global, inside the slab) as nx-wide row-major images. */
 int svr_read_coronal(svr_volume* vol, int32_t z0, int32_t z1, float* mean_out, float* max_out,
                      int32_t* depth_out);

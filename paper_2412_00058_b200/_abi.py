@@ -111,6 +111,7 @@ SIGNATURES = {
     "svr_frame_step": (C.c_int, [P, P, I64, PR, PC, I32, C.POINTER(RenderParams), PB]),
     "svr_read_coronal": (C.c_int, [P, I32, I32, P, P, P]),
     "svr_read_coronal_async": (C.c_int, [P, I32, I32, P, P, P]),
+    "svr_set_gather_targets": (C.c_int, [P, C.POINTER(P), I32, I32, I32]),
     "svr_coronal_projection": (C.c_int, [P, I32, I32, I32, P]),
     "svr_read_accumulators": (C.c_int, [P, PB, P, P]),
     "svr_read_values": (C.c_int, [P, PB, I32, P]),

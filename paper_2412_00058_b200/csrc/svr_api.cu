@@ -121,6 +121,8 @@ struct svr_volume {
     uint64_t frames = 0;
     ull* d_work = nullptr;          // deferred exact-path chunks of k_pnn_plane
     FrameGraph fg;                  // svr_frame_step graph
+    GatherTargets gt{nullptr, 0, 0, 0, 0};  // fused render + gather targets (device pointer array)
+    float** d_gt = nullptr;
     void* d_tiles = nullptr;        // region tables of the multi-box fill / render launches
     size_t tiles_cap = 0;
     unsigned int* d_work_n = nullptr;
@@ -645,6 +647,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFree(v->d_work);
     cudaFree(v->d_tiles);
     cudaFree(v->d_work_n);
+    cudaFree(v->d_gt);
     if (v->fg.exec) cudaGraphExecDestroy(v->fg.exec);
     if (v->fg.graph) cudaGraphDestroy(v->fg.graph);
     if (v->fg.done) cudaEventDestroy(v->fg.done);
@@ -1511,7 +1514,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
     CKL();
     k_band<<<grid_1d(nm), 128, 0, v->stream>>>(v->acc, v->fill, g, dmt, (int)mt.size(), p->median_radius,
                                                 above, below, p->fill_mode, v->r_depth, v->r_mdepth,
-                                                v->r_mean, v->r_max);
+                                                v->r_mean, v->r_max, v->gt);
     v->launches++;
     CKL();
     return SVR_OK;
@@ -1853,7 +1856,7 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
                                                                   p.fill_mode, v->r_depth);
         k_band<<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, mt, 1, p.median_radius, above,
                                                              below, p.fill_mode, v->r_depth, v->r_mdepth,
-                                                             v->r_mean, v->r_max);
+                                                             v->r_mean, v->r_max, v->gt);
     }
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(v->stream, &graph);
@@ -1955,5 +1958,24 @@ extern "C" int svr_selftest_value_rounding(int device, int64_t* mismatches) {
     CK(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
     cudaFree(d);
     *mismatches = (int64_t)h;
+    return SVR_OK;
+}
+
+extern "C" int svr_set_gather_targets(svr_volume* v, void* const* images, int32_t n, int32_t own_z0,
+                                      int32_t own_z1) {
+    VOL_CHECK(v);
+    if (n < 0 || n > 64 || (n > 0 && !images)) return fail(SVR_E_INVALID, "invalid gather target list");
+    if (n > 0 && (own_z0 < v->d.z_begin || own_z1 > v->d.z_end || own_z0 >= own_z1))
+        return fail(SVR_E_INVALID, "owned rows [%d,%d) outside the slab [%d,%d)", own_z0, own_z1,
+                    v->d.z_begin, v->d.z_end);
+    CK(cudaStreamSynchronize(v->stream));
+    cudaFree(v->d_gt);
+    v->d_gt = nullptr;
+    v->gt = GatherTargets{nullptr, 0, 0, 0, 0};
+    if (n == 0) return SVR_OK;
+    CK(cudaMalloc(&v->d_gt, sizeof(float*) * n));
+    CK(cudaMemcpy(v->d_gt, images, sizeof(float*) * n, cudaMemcpyHostToDevice));
+    v->gt = GatherTargets{v->d_gt, n, own_z0, own_z1, (long long)v->d.nz * v->d.nx};
+    if (v->fg.ready) v->fg.ready = false;  // the frame graph captured the old targets
     return SVR_OK;
 }

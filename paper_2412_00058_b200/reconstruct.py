@@ -182,6 +182,15 @@ class VoxelGrid:
         check(lib().svr_render_coronal(self._h, C.byref(_box(dirty)) if dirty is not None else None,
                                        fill_radius, C.byref(params)))
 
+    def set_gather_targets(self, images, own=None):
+        """Fused render + gather: later renders also store the owned rows' mean / max into each
+        image (device tensors or pointers of [2, nz, nx] f32, e.g. symmetric-memory peers).
+        images = [] switches it off.  own = (z0, z1) owned global rows (default: the slab)."""
+        ptrs = [ptr(t) for t in images]
+        arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
+        z0, z1 = own if own is not None else (self.desc.z_begin, self.desc.z_end)
+        check(lib().svr_set_gather_targets(self._h, arr, len(ptrs), int(z0), int(z1)))
+
     def read_coronal(self, z0=None, z1=None):
         z0 = self.desc.z_begin if z0 is None else z0
         z1 = self.desc.z_end - 1 if z1 is None else z1

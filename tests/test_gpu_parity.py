@@ -397,9 +397,26 @@ def test_slab_sharded_bench_step_equals_unsharded(world):
     mean_f, max_f, dep_f = full.read_coronal()
     slabs = sharding.plan_slabs(wl.dims[2], world, fill_r + rp.median_radius)
     boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    # fused render + gather: each "rank" stores its owned rows into every rank's full image
+    # (here ordinary device buffers stand in for the ranks' symmetric-memory peers)
+    import torch
+    images = [torch.zeros((2, wl.dims[2], wl.dims[0]), dtype=torch.float32, device="cuda")
+              for _ in range(world)]
+
+    def run(z_range, idx, own=None):
+        boxes_ = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+        g = _grid(wl, z_range=z_range)
+        if own is not None:
+            g.set_gather_targets(images, own)
+        g.insert_frames(frames[idx], wl.poses[idx], wl.calib)
+        g.fill_holes_boxes(sharding.chunk_boxes(boxes_, idx, z_range, chunk=32, dilate=fill_r), fill_r,
+                           pkg.FILL_MEAN, count=False)
+        g.render_coronal_boxes(sharding.chunk_boxes(boxes_, idx, z_range, chunk=32), rp, fill_r)
+        return g
+
     for sl in slabs:
         idx = sharding.route(boxes, sl.alloc)
-        g = run(sl.alloc, idx)
+        g = run(sl.alloc, idx, own=sl.owned)
         o0, o1 = sl.owned
         s, c = g.accumulators((0, 0, o0, wl.dims[0] - 1, wl.dims[1] - 1, o1 - 1))
         assert np.array_equal(c, c_full[o0:o1]) and np.array_equal(s, s_full[o0:o1])
@@ -407,6 +424,9 @@ def test_slab_sharded_bench_step_equals_unsharded(world):
         assert np.array_equal(m, mean_f[o0:o1]) and np.array_equal(x, max_f[o0:o1])
         assert np.array_equal(d, dep_f[o0:o1])
         del g
+    torch.cuda.synchronize()
+    for img in images:
+        assert np.array_equal(img[0].cpu().numpy(), mean_f) and np.array_equal(img[1].cpu().numpy(), max_f)
 
 
 @pytest.mark.parametrize("source", ["host", "device", "pinned"])
