@@ -176,6 +176,8 @@ def test_incremental_equals_batch():
 
 
 def test_order_independence():
+    """SPEC.md:327 / :645: any permutation of the inserts gives identical accumulators (100
+    shuffles of a small scan, plus a cfg1 shuffle), one frame per call and in batches."""
     wl = synth.cfg1(nframes=50)
     frames = wl.frames_np()
     a = _grid(wl)
@@ -185,6 +187,75 @@ def test_order_independence():
     b.insert_frames(frames[perm], wl.poses[perm], wl.calib)
     for x, y in zip(a.accumulators(), b.accumulators()):
         assert np.array_equal(x, y)
+    sl = synth.small_linear(nframes=12)
+    fr = sl.frames_np()
+    ref = _grid(sl)
+    ref.insert_frames(fr, sl.poses, sl.calib)
+    s0, c0 = ref.accumulators()
+    rng = np.random.default_rng(1)
+    g = _grid(sl)
+    for shuffle in range(100):
+        g.clear()
+        p = rng.permutation(sl.nframes)
+        if shuffle % 2:
+            for k in p:
+                g.insert_frames(fr[k], sl.poses[k:k + 1], sl.calib)
+        else:
+            g.insert_frames(fr[p], sl.poses[p], sl.calib)
+        s1, c1 = g.accumulators()
+        assert np.array_equal(c1, c0) and np.array_equal(s1, s0), shuffle
+
+
+def test_spec_full_frame_rebinning_and_mean_bound():
+    """one full 559 x 699 frame (0.1 mm/px) into 1 mm voxels -- counts and sums equal
+    the brute-force re-binning (the oracle); every voxel value lies within the [min, max]
+    of the pixel values inserted (frames drawn from [40, 90])."""
+    rng = np.random.default_rng(7)
+    calib = synth.linear_calib(559, 699, 0.1, 0.1)
+    frames = rng.integers(40, 91, (3, 699, 559), dtype=np.uint8)
+    poses = np.zeros(3, dtype=synth._abi.RIGID_DTYPE)
+    for k in range(3):
+        q = synth.quat_normalized(synth.quat_mul(synth.quat_axis_angle((1, 0, 0), 0.3 + 0.1 * k),
+                                                 synth.quat_axis_angle((0, 0, 1), 0.05 * k)))
+        poses[k] = (*q, 2.0 + k, 3.0, 20.0 + 0.7 * k)
+    dims, vox, org = (64, 72, 64), 1.0, (0.0, 0.0, 0.0)
+    g = pkg.VoxelGrid(dims, vox, org, device=0)
+    g.insert_frames(frames, poses, calib)
+    ref = O.OracleGrid(dims, vox, org)
+    ref.insert_frames(frames, poses, calib)
+    s, c = g.accumulators()
+    assert np.array_equal(c, ref.count) and np.array_equal(s, ref.sum)
+    assert int(c.sum()) == g.stats()["pixels_inserted"] > 0
+    v = g.values()
+    assert v[c > 0].min() >= 40 and v[c > 0].max() <= 90
+
+
+def test_incremental_300_frames_throughput_floor():
+    """SPEC.md:313 / :638-639: a 300-frame scan of 559 x 699 frames into a 1 mm grid of
+    >= 500 x 100 x 70 mm, frame by frame (insert -> fill -> render as one graph replay each), equals
+    the batch result, at far more than the 30 frames/s floor."""
+    import time
+    calib = synth.linear_calib(559, 699, 0.1, 0.1)
+    rng = np.random.default_rng(8)
+    n = 300
+    frames = rng.integers(0, 256, (n, 699, 559), dtype=np.uint8)
+    poses = np.zeros(n, dtype=synth._abi.RIGID_DTYPE)
+    for k in range(n):
+        q = synth.quat_normalized(synth.quat_axis_angle((1, 0, 0), np.radians(rng.uniform(-3, 3))))
+        poses[k] = (*q, 10.0 + rng.uniform(-1, 1), 5.0, 10.0 + 1.6 * k)
+    dims, vox, org = (500, 100, 520), 1.0, (0.0, 0.0, 0.0)
+    rp = synth.render_params(depth_lo_mm=10.0, depth_hi_mm=60.0)
+    inc = pkg.VoxelGrid(dims, vox, org, device=0)
+    t0 = time.perf_counter()
+    pkg.run_incremental(frames, poses, calib, inc, 1, pkg.FILL_MEAN, render=rp)
+    fps = n / (time.perf_counter() - t0)
+    bat = pkg.VoxelGrid(dims, vox, org, device=0)
+    _, u = bat.insert_frames(frames, poses, calib, want_boxes=True)
+    bat.fill_holes(pkg.dilate(u, 1), 1, pkg.FILL_MEAN)
+    for a, b in zip(inc.accumulators(), bat.accumulators()):
+        assert np.array_equal(a, b)
+    assert np.array_equal(inc.fill_layer(), bat.fill_layer())
+    assert fps >= 30.0, fps
 
 
 def test_projection_u8():
