@@ -13,12 +13,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "svr_host.hpp"
 #include "svr_kernels.cuh"
 
 using namespace svr;
 
 static thread_local std::string g_err;
+
+// NVTX range over a C-ABI call (header-only NVTX3: free unless a profiler is attached), so
+// nsys / ncu range filters see insert / fill / render / frame_step by name.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 static int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -1179,6 +1188,7 @@ extern "C" int svr_insert_frames(svr_volume* v, const uint8_t* px, int64_t pitch
                                  int32_t w, int32_t h, int32_t n, const svr_rigid* poses,
                                  const svr_calib* c, int32_t skip_zero, svr_box* dirty_out,
                                  svr_box* union_out) {
+    NvtxRange nvtx_("svr_insert_frames");
     VOL_CHECK(v);
     const bool want_box = dirty_out || union_out;
     const int mode = v->d.accum == SVR_ACC_TRILINEAR ? kModeTrilinear : kModeInsert;
@@ -1403,6 +1413,7 @@ static int finish_count(svr_volume* v, int64_t* filled_out) {
 
 extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode, int32_t radius,
                               int64_t* filled_out) {
+    NvtxRange nvtx_("svr_fill_holes");
     VOL_CHECK(v);
     if (int e = check_fill_args(v, mode, radius)) return e;
     Box b;
@@ -1416,6 +1427,7 @@ extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode
 
 extern "C" int svr_fill_holes_boxes(svr_volume* v, const svr_box* regions, int32_t n, int32_t mode,
                                     int32_t radius, int64_t* filled_out) {
+    NvtxRange nvtx_("svr_fill_holes_boxes");
     VOL_CHECK(v);
     if (int e = check_fill_args(v, mode, radius)) return e;
     if (n < 0 || (n > 0 && !regions)) return fail(SVR_E_INVALID, "bad region list");
@@ -1522,12 +1534,14 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
 
 extern "C" int svr_render_coronal(svr_volume* v, const svr_box* dirty, int32_t fill_radius,
                                   const svr_render_params* p) {
+    NvtxRange nvtx_("svr_render_coronal");
     VOL_CHECK(v);
     return render_boxes(v, dirty, dirty ? 1 : 0, fill_radius, p);
 }
 
 extern "C" int svr_render_coronal_boxes(svr_volume* v, const svr_box* dirty, int32_t n,
                                         int32_t fill_radius, const svr_render_params* p) {
+    NvtxRange nvtx_("svr_render_coronal_boxes");
     VOL_CHECK(v);
     if (n <= 0 || !dirty) return n == 0 ? SVR_OK : fail(SVR_E_INVALID, "bad region list");
     return render_boxes(v, dirty, n, fill_radius, p);
@@ -1896,6 +1910,7 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
 extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, const svr_rigid* pose,
                               const svr_calib* c, int32_t fill_radius, const svr_render_params* p,
                               svr_box* dirty_out) {
+    NvtxRange nvtx_("svr_frame_step");
     VOL_CHECK(v);
     if (!v->acc) return fail(SVR_E_INVALID, "frame step needs a PNN volume");
     if (!px || !pose || !p) return fail(SVR_E_INVALID, "NULL argument");
