@@ -214,6 +214,11 @@ int svr_coronal_projection(svr_volume* vol, int32_t mode, int32_t depth_axis, in
 /* Accumulator / value readout over an inclusive box (NULL = whole slab), x fastest. */
 int svr_read_accumulators(svr_volume* vol, const svr_box* box, uint32_t* sum_out,
                           uint16_t* count_out);
+/* Checkpoint / resume: overwrite the accumulators of a box (NULL = whole slab) from sum / count
+ * arrays in the svr_read_accumulators layout (host or device).  Re-inserting further frames after a
+ * restore gives the uninterrupted result (inserts commute). */
+int svr_write_accumulators(svr_volume* vol, const svr_box* box, const uint32_t* sum,
+                           const uint16_t* count);
 /* VoxelGrid::value = round(sum/count); apply_fills adds rounded fill values. */
 int svr_read_values(svr_volume* vol, const svr_box* box, int32_t apply_fills, uint8_t* out);
 /* export_slices along x: nx images of ny x nzl u8 values (row = z, column =

@@ -115,6 +115,7 @@ SIGNATURES = {
     "svr_coronal_projection": (C.c_int, [P, I32, I32, I32, P]),
     "svr_read_accumulators": (C.c_int, [P, PB, P, P]),
     "svr_read_values": (C.c_int, [P, PB, I32, P]),
+    "svr_write_accumulators": (C.c_int, [P, PB, P, P]),
     "svr_read_fill": (C.c_int, [P, PB, P]),
     "svr_read_trilinear": (C.c_int, [P, PB, P, P]),
     "svr_get_stats": (C.c_int, [P, PS]),

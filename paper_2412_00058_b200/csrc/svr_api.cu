@@ -1638,6 +1638,29 @@ extern "C" int svr_read_accumulators(svr_volume* v, const svr_box* box, uint32_t
     return SVR_OK;
 }
 
+extern "C" int svr_write_accumulators(svr_volume* v, const svr_box* box, const uint32_t* sum,
+                                      const uint16_t* cnt) {
+    VOL_CHECK(v);
+    if (!v->acc) return fail(SVR_E_INVALID, "not a PNN volume");
+    if (!sum || !cnt) return fail(SVR_E_INVALID, "sum and count are required");
+    Box b;
+    long long n;
+    if (int e = read_box_common(v, box, &b, &n)) return e;
+    uint32_t* ts = nullptr;
+    uint16_t* tc = nullptr;
+    CK(cudaMallocAsync(&ts, n * 4, v->stream));
+    CK(cudaMallocAsync(&tc, n * 2, v->stream));
+    CK(cudaMemcpyAsync(ts, sum, n * 4, cudaMemcpyDefault, v->stream));
+    CK(cudaMemcpyAsync(tc, cnt, n * 2, cudaMemcpyDefault, v->stream));
+    k_write_acc<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, dev_grid(v->d), b, ts, tc);
+    v->launches++;
+    CKL();
+    CK(cudaFreeAsync(ts, v->stream));
+    CK(cudaFreeAsync(tc, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    return SVR_OK;
+}
+
 extern "C" int svr_read_values(svr_volume* v, const svr_box* box, int32_t apply_fills, uint8_t* out) {
     VOL_CHECK(v);
     if (!v->acc) return fail(SVR_E_INVALID, "not a PNN volume");

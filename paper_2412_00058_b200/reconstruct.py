@@ -230,6 +230,30 @@ class VoxelGrid:
         check(lib().svr_read_accumulators(self._h, C.byref(b), ptr(s), ptr(c)))
         return s, c
 
+    def set_accumulators(self, sum_, count, box=None):
+        """Restore sum / count (the `accumulators()` layout) into `box` (default: the slab)."""
+        b, shp = self._box_shape(box)
+        s = np.ascontiguousarray(sum_, np.uint32).reshape(shp)
+        c = np.ascontiguousarray(count, np.uint16).reshape(shp)
+        check(lib().svr_write_accumulators(self._h, C.byref(b), ptr(s), ptr(c)))
+
+    def save(self, path):
+        """Checkpoint the accumulators (npz with the grid description); fills are derived state."""
+        s, c = self.accumulators()
+        d = self.desc
+        np.savez_compressed(path, sum=s, count=c, dims=np.array([d.nx, d.ny, d.nz]),
+                            voxel_mm=d.voxel_mm, origin=np.array(list(d.origin_mm)),
+                            z_range=np.array([d.z_begin, d.z_end]))
+
+    def load(self, path):
+        """Resume from `save`: the grid description must match."""
+        z = np.load(path)
+        d = self.desc
+        if list(z["dims"]) != [d.nx, d.ny, d.nz] or list(z["z_range"]) != [d.z_begin, d.z_end] or \
+                float(z["voxel_mm"]) != d.voxel_mm:
+            raise InvalidInput("checkpoint does not match this grid")
+        self.set_accumulators(z["sum"], z["count"])
+
     def values(self, box=None, apply_fills=False):
         """VoxelGrid::value (SPEC.md:277) = round(sum/count), 0 when empty."""
         b, shp = self._box_shape(box)

@@ -581,3 +581,23 @@ def test_value_rounding_selftest():
     bad = C.c_int64(-1)
     _abi.check(_abi.lib().svr_selftest_value_rounding(0, C.byref(bad)))
     assert bad.value == 0
+
+
+def test_checkpoint_resume(tmp_path):
+    """Accumulator checkpoint / resume: save mid-scan, restore into a fresh grid,
+    insert the rest -> identical to the uninterrupted scan."""
+    wl = synth.cfg1(nframes=40)
+    frames = wl.frames_np()
+    full = _grid(wl)
+    full.insert_frames(frames, wl.poses, wl.calib)
+    a = _grid(wl)
+    a.insert_frames(frames[:17], wl.poses[:17], wl.calib)
+    a.save(tmp_path / "ck.npz")
+    b = _grid(wl)
+    b.load(tmp_path / "ck.npz")
+    b.insert_frames(frames[17:], wl.poses[17:], wl.calib)
+    for x, y in zip(b.accumulators(), full.accumulators()):
+        assert np.array_equal(x, y)
+    other = pkg.VoxelGrid((8, 8, 8), 1.0, (0, 0, 0), device=0)
+    with pytest.raises(pkg.InvalidInput):
+        other.load(tmp_path / "ck.npz")
