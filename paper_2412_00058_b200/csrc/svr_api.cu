@@ -1009,6 +1009,9 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             const int ntx = (cpr + kPlaneTW - 1) / kPlaneTW, nty = (h + kPlaneTH - 1) / kPlaneTH;
             dim3 grid(ntx, m, nty), grid6((cpr + 5) / 6, m, nty);
             const int tw = v->plane_tw_cur;
+            // the deferred-chunk pass is grid-strided over a worklist of a few entries per frame:
+            // a single frame must not pay for launching thousands of idle CTAs
+            const int work_ctas = std::min(4096, std::max(16, 8 * m));
             const GridDev gd = dev_grid(v->d);
 #define LP(a, b, c)                                                                               \
     if (tw == 6)                                                                                  \
@@ -1021,7 +1024,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                                                       cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,  \
                                                       v->d_work_n, v->work_cap, 1u << 20,          \
                                                       v->plane_prefetch);                          \
-    k_pnn_work<a, b><<<4096, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,     \
+    k_pnn_work<a, b><<<work_ctas, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,\
                                                      gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
                                                      v->work_cap)
             if (v->plane_walk) {
