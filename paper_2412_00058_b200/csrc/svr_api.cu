@@ -1890,9 +1890,9 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
     const ColTiles* dt = (const ColTiles*)(f.d_tiles + sizeof(BoxTiles));
     const ColTiles* mt = dt + 1;
     if (!e) {
-        // 4-plane marches: a single frame's box is shallow in z, short marches cut its latency
-        k_fill_warp<4, 1, 8><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, v->d_counter);
-        k_depth<4><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, dt, 1, ylo, yhi,
+        // 2-plane marches: a single frame's box is shallow in z, short marches cut its latency
+        k_fill_warp<2, 1, 8><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, v->d_counter);
+        k_depth<8><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, dt, 1, ylo, yhi,
                                                                   p.fill_mode, v->r_depth);
         k_band<<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, mt, 1, p.median_radius, above,
                                                              below, p.fill_mode, v->r_depth, v->r_mdepth,
@@ -1962,9 +1962,9 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     bt.ntx = (fb.x1 - fb.x0 + 1 + 119) / 120;
     bt.nty = (fb.y1 - fb.y0 + 1 + 7) / 8;
     bt.first = 0;
-    const long long nf = (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 3) / 4);
+    const long long nf = (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 1) / 2);
     std::vector<ColTiles> cv{ct[0]}, mv{ct[1]};
-    const long long nd = tile_cols(cv, 32), nm = tile_cols(mv);
+    const long long nd = tile_cols(cv, 16), nm = tile_cols(mv);
     if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm))
         if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;
     if (int e = make_params(*pose, prep_ctx(*c, v->d), c->scale_x_mm, c->scale_y_mm, f.h_fp)) return e;
