@@ -138,7 +138,7 @@ struct svr_volume {
     unsigned int work_cap = 0;
     int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
     int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 step counters, 0 carries
-    int depth_seg = 4;          // SVR_DEPTH_SEG: threads per column in k_depth (4, or 1)
+    int depth_seg = 4;          // SVR_DEPTH_SEG: threads per column in k_depth (4; 8 or 1 A/B)
     int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
     int plane_tw_cur = 4;       // the width chosen for the current insert call
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
@@ -703,7 +703,10 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         v->fill_ty = (t == 4 || t == 12 || t == 16) ? t : 8;
     }
     if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
-    if (const char* e = std::getenv("SVR_DEPTH_SEG")) v->depth_seg = std::atoi(e) == 4 ? 4 : 1;
+    if (const char* e = std::getenv("SVR_DEPTH_SEG")) {
+        const int sg = std::atoi(e);
+        v->depth_seg = (sg == 1 || sg == 8) ? sg : 4;
+    }
     if (const char* e = std::getenv("SVR_PLANE_TW")) v->plane_tw = std::atoi(e) == 6 ? 6 : 4;
     if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
@@ -1519,7 +1522,10 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
     const ColTiles* ddt = (const ColTiles*)d;
     const ColTiles* dmt = ddt + dt.size();
     const GridDev g = dev_grid(v->d);
-    if (v->depth_seg == 4)
+    if (v->depth_seg == 8)
+        k_depth<8><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
+                                                        p->fill_mode, v->r_depth);
+    else if (v->depth_seg == 4)
         k_depth<4><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
                                                         p->fill_mode, v->r_depth);
     else
