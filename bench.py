@@ -247,7 +247,7 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.fused_gather_1:
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
@@ -305,13 +305,15 @@ def run_ours(args):
     rows = own[1] - own[0]
     rows_max = max(oe[r] - ob[r] for r in range(world))
     gath_src = torch.zeros((2, rows_max, wl.dims[0]), dtype=torch.float32, device=dev)
-    gath_dst = torch.zeros((world, 2, rows_max, wl.dims[0]), dtype=torch.float32, device=dev) if world > 1 else None
+    fused_try = (world > 1 or args.fused_gather_1) and not args.nccl_gather
+    gath_dst = torch.zeros((world, 2, rows_max, wl.dims[0]), dtype=torch.float32, device=dev) \
+        if world > 1 or fused_try else None
 
     # Fused render + gather: with symmetric memory (NVLink / NVSwitch peer mappings) every rank's
     # band kernel stores its owned rows straight into all ranks' full images and a device-side
     # barrier replaces the all-gather.  Verified once against the NCCL gather; falls back to it.
     gather_mode, gather_note, symm_h, full_img = "nccl", "", None, None
-    if world > 1 and not args.nccl_gather:
+    if fused_try:
         try:
             import torch.distributed._symmetric_memory as symm
             full_img = symm.empty((2, nz, wl.dims[0]), dtype=torch.float32, device=dev)
@@ -324,12 +326,11 @@ def run_ours(args):
             symm_h = None
 
     def gather():
-        if world > 1:
-            if gather_mode == "fused-p2p":
-                symm_h.barrier(0)
-            else:
-                grid.read_coronal_into(own[0], own[1] - 1, gath_src[0], gath_src[1])
-                dist.all_gather_into_tensor(gath_dst, gath_src)
+        if gather_mode == "fused-p2p":
+            symm_h.barrier(0)
+        elif world > 1:
+            grid.read_coronal_into(own[0], own[1] - 1, gath_src[0], gath_src[1])
+            dist.all_gather_into_tensor(gath_dst, gath_src)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.warmup + args.steps)]
 
@@ -503,7 +504,7 @@ def run_ours(args):
         "data": "synthetic (seeded Rayleigh speckle + vertebra arcs, BASELINE cfg2 generator)",
         "config": {"workload": WORKLOAD, "frames": wl.nframes, "frame": [wl.h, wl.w],
                    "grid": list(wl.dims), "voxel_mm": wl.voxel_mm, "parallelism": "z-slab x%d" % world,
-                   "gather": gather_mode if world > 1 else None, "gather_note": gather_note or None,
+                   "gather": gather_mode if world > 1 or fused_try else None, "gather_note": gather_note or None,
                    "l2": "no flush: frames (590 MB) and volume (2.1 GB) exceed the 126 MB L2",
                    "frames_this_rank": int(n_my)},
         "stages_ms": {"insert": ins_ms, "fill": fill_ms, "render": rend_ms},
@@ -554,6 +555,8 @@ def main():
     ap.add_argument("--no-other-configs", action="store_true", help="skip cfg1/cfg3/cfg5 lines")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N>1: gather the coronal strips with NCCL instead of the fused peer stores")
+    ap.add_argument("--fused-gather-1", action="store_true",
+                    help="exercise the fused peer-store gather (symmetric memory + device barrier) at N=1 too")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
