@@ -372,6 +372,31 @@ def test_mean_fill_kernels_bitexact(fill_kernel, monkeypatch):
         assert np.array_equal(grid.fill_layer(), ref.fill), region
 
 
+@pytest.mark.parametrize("fill_kernel", ["tma", "warp", "smem"])
+def test_fill_large_accumulators(fill_kernel, monkeypatch):
+    """Voxel values from counts up to the u16 maximum and sums past 2^23 (outside the fp32
+    estimate's exact range: the fill kernels' recompute path) feed the neighbours' mean fills
+    exactly as in the oracle."""
+    monkeypatch.setenv("SVR_FILL_KERNEL", fill_kernel)
+    dims = (70, 40, 50)
+    rng = np.random.default_rng(21)
+    shp = (dims[2], dims[1], dims[0])
+    count = np.where(rng.random(shp) < 0.4, rng.integers(1, 65536, shp), 0).astype(np.uint16)
+    big = rng.random(shp) < 0.5
+    mean = np.where(big, rng.integers(128, 256, shp), rng.integers(0, 256, shp))
+    sum_ = (count.astype(np.uint64) * mean + rng.integers(0, 2, shp) * (count > 1)).astype(np.uint32)
+    assert (sum_ >= (1 << 23)).any()
+    grid = pkg.VoxelGrid(dims, 1.0, (0, 0, 0), device=0)
+    grid.set_accumulators(sum_, count)
+    ref = O.OracleGrid(dims, 1.0)
+    ref.sum[...] = sum_
+    ref.count[...] = count
+    for region in (None, (5, 3, 2, 60, 30, 45)):
+        assert grid.fill_holes(region, 1, pkg.FILL_MEAN) == ref.fill_holes(region, 0, 1)
+        assert np.array_equal(grid.fill_layer(), ref.fill), region
+    assert np.array_equal(grid.values(apply_fills=True), ref.values(apply_fills=True))
+
+
 def test_chunked_dirty_regions_equal_bounding_box():
     """Batch fill/render over per-z-chunk dirty boxes (svr_fill_holes_boxes,
     svr_render_coronal_boxes) equals the same over one bounding box, bit for bit."""
