@@ -1304,7 +1304,7 @@ static bool fill_tmap(svr_volume* v) {
     return true;
 }
 
-static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, int32_t radius) {
+static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, int32_t radius, bool count) {
     const GridDev g = dev_grid(v->d);
     if (mode == SVR_FILL_MEAN && radius == 1 && v->fill_tma && !v->fill_smem && fill_tmap(v)) {
         const int zc = v->fill_tma_zc;
@@ -1363,6 +1363,8 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
             FW(16, 1, 16);
         } else {
             if (zc == 8) FW(8, 1, 8);
+            else if (zc == 32 && !count)
+                k_fill_warp<32, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
             else if (zc == 32) FW(32, 1, 8);
             else FW(16, 1, 8);
         }
@@ -1427,7 +1429,7 @@ extern "C" int svr_fill_holes(svr_volume* v, const svr_box* region, int32_t mode
     if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
     v->fill_mode = mode;
     if (any)
-        if (int e = fill_boxes(v, std::vector<Box>{b}, mode, radius)) return e;
+        if (int e = fill_boxes(v, std::vector<Box>{b}, mode, radius, filled_out != nullptr)) return e;
     return finish_count(v, filled_out);
 }
 
@@ -1445,7 +1447,7 @@ extern "C" int svr_fill_holes_boxes(svr_volume* v, const svr_box* regions, int32
     if (filled_out) CK(cudaMemsetAsync(v->d_counter, 0, sizeof(ull), v->stream));
     v->fill_mode = mode;
     if (!bs.empty())
-        if (int e = fill_boxes(v, bs, mode, radius)) return e;
+        if (int e = fill_boxes(v, bs, mode, radius, filled_out != nullptr)) return e;
     return finish_count(v, filled_out);
 }
 
@@ -1897,7 +1899,7 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
     const ColTiles* mt = dt + 1;
     if (!e) {
         // 2-plane marches: a single frame's box is shallow in z, short marches cut its latency
-        k_fill_warp<2, 1, 8><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, v->d_counter);
+        k_fill_warp<2, 1, 8, false><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, nullptr);
         k_depth<8><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, dt, 1, ylo, yhi,
                                                                   p.fill_mode, v->r_depth);
         k_band<<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, mt, 1, p.median_radius, above,
