@@ -244,7 +244,9 @@ int svr_count_footprint(svr_volume* vol, const uint8_t* px, int64_t row_pitch,
                         int64_t* distinct_out);
 
 /* Self-test of the device VoxelGrid::value rounding: checks every count in [1, 255] and every
- * reachable sum against integer division; writes the mismatch count (0 expected). */
+ * reachable sum against integer division, and the render's branch-free fill-layer division
+ * (payload / n) against IEEE division for every payload in [0, 65535] and n in [1, 1024];
+ * writes the mismatch count (0 expected). */
 int svr_selftest_value_rounding(int device, int64_t* mismatches);
 
 /* Synthetic B-scan generator (bench input, BASELINE configs): writes nframes frames of

@@ -2002,6 +2002,7 @@ extern "C" int svr_selftest_value_rounding(int device, int64_t* mismatches) {
     CK(cudaMalloc(&d, sizeof(unsigned long long)));
     CK(cudaMemset(d, 0, sizeof(unsigned long long)));
     k_selftest_value<<<255, 256>>>(d);
+    k_selftest_div<<<1024, 256>>>(d);
     CKL();
     unsigned long long h = 0;
     CK(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
