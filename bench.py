@@ -410,6 +410,16 @@ def run_ours(args):
         e2e_s = allmax(time.perf_counter() - w0)
         h2d = n_my * px_frame + n_my * 224
         d2h = 2 * rows * wl.dims[0] * 4
+        # the host link's own ceiling: the same pinned frames copied alone (best of 2, CUDA events)
+        link_ms = []
+        for _ in range(2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            frames.copy_(frames_host, non_blocking=True)  # identical bytes: frames_host = frames
+            b.record(stream)
+            b.synchronize()
+            link_ms.append(a.elapsed_time(b))
+        link_gbs = frames_host.numel() / (min(link_ms) * 1e-3) / 1e9 if n_my else None
 
         # ---- per-frame incremental latency (insert -> fill(box+1) -> render(box)), rank-local:
         # the product path is svr_frame_step (one CUDA-graph replay per frame); the per-call
@@ -525,7 +535,11 @@ def run_ours(args):
                                     "wall_p50": pct(lat_wall_c, 0.5),
                                     "what": "the same kernels launched call by call"}},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                "link": {"h2d_gbs_achieved": h2d * e2e_steps / e2e_s / 1e9,
+                         "h2d_gbs_copy_alone": link_gbs,
+                         "frac": (h2d * e2e_steps / e2e_s / 1e9) / link_gbs if link_gbs else None,
+                         "what": "e2e H2D bytes / e2e time vs the same pinned frames copied alone"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "cpu_baseline": cpu,
