@@ -598,6 +598,26 @@ def test_edge_cases():
     assert np.array_equal(slab.values(), full.values()[10:30])
 
 
+def test_count_cap_flagged_at_readout():
+    """SPEC.md:336 caps: past 65534 pixels in one voxel the oracle drops pixels one by one; the
+    device keeps counting (order-independent atomics) and the readout clamps the count to the
+    u16 maximum and reports the voxel as saturated (DESIGN.md §3 caps row)."""
+    from paper_2412_00058_b200 import _abi
+    calib = synth.linear_calib(16, 16, 0.1, 0.1)
+    frames = np.full((300, 16, 16), 200, np.uint8)  # 300 x 256 px, all into voxel (1, 1, 1)
+    poses = np.zeros(300, dtype=_abi.RIGID_DTYPE)
+    poses["qw"] = 1.0
+    poses["tx"] = poses["ty"] = poses["tz"] = 12.0
+    g = pkg.VoxelGrid((3, 3, 3), 10.0, (0.0, 0.0, 0.0), device=0)
+    g.insert_frames(frames, poses, calib)
+    s, c = g.accumulators()
+    assert c[1, 1, 1] == 65535 and g.stats()["pixels_saturated"] >= 1
+    assert int(c.sum()) == 65535 and g.values()[1, 1, 1] == 200
+    ref = O.OracleGrid((3, 3, 3), 10.0)
+    ref.insert_frames(frames, poses, calib)
+    assert ref.count[1, 1, 1] == 65534 and ref.stats["saturated"] == 300 * 256 - 65534
+
+
 def test_value_rounding_selftest():
     """Device acc_value (round(sum / count) via an approximate divide + 1/2 offset) equals
     integer division for every count in [1, 255] and every reachable sum."""
