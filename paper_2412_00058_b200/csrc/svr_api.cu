@@ -1338,8 +1338,8 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         for (const Box& b : bs) {
             BoxTiles t;
             t.b = b;
-            t.ntx = (b.x1 - b.x0 + 1 + 119) / 120;
-            t.nty = (b.y1 - b.y0 + 1 + v->fill_ty - 1) / v->fill_ty;
+            t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of fill_ty rows
+            t.nty = (b.y1 - b.y0 + 1 + 4 * v->fill_ty - 1) / (4 * v->fill_ty);
             t.first = total;
             total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
             bt.push_back(t);
@@ -1967,8 +1967,8 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     }
     BoxTiles bt;
     bt.b = fb;
-    bt.ntx = (fb.x1 - fb.x0 + 1 + 119) / 120;
-    bt.nty = (fb.y1 - fb.y0 + 1 + 7) / 8;
+    bt.ntx = (fb.x1 - fb.x0 + 1 + 29) / 30;  // k_fill_warp<.., 8>: 30 columns x 4 warps of 8 rows
+    bt.nty = (fb.y1 - fb.y0 + 1 + 31) / 32;
     bt.first = 0;
     const long long nf = (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 1) / 2);
     std::vector<ColTiles> cv{ct[0]}, mv{ct[1]};
