@@ -141,6 +141,7 @@ struct svr_volume {
     int depth_seg = 4;          // SVR_DEPTH_SEG: threads per column in k_depth (4; 8 or 1 A/B)
     int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
     int plane_tw_cur = 4;       // the width chosen for the current insert call
+    int plane_flush_lin = 1;    // SVR_PLANE_FLUSH: k_pnn_lin table flush, 1 linear over all threads, 0 lane = x
     int plane_lin = 1;          // SVR_PLANE_LIN: k_pnn_lin for linear probes (1: 128-row tiles, 2: 64), 0 k_pnn_plane
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
@@ -709,7 +710,8 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         v->depth_seg = (sg == 1 || sg == 8) ? sg : 4;
     }
     if (const char* e = std::getenv("SVR_PLANE_TW")) v->plane_tw = std::atoi(e) == 6 ? 6 : 4;
-    if (const char* e = std::getenv("SVR_PLANE_LIN")) v->plane_lin = std::min(2, std::max(0, std::atoi(e)));
+    if (const char* e = std::getenv("SVR_PLANE_FLUSH")) v->plane_flush_lin = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("SVR_PLANE_LIN")) v->plane_lin = std::min(3, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
         v->insert_kernel = !std::strcmp(e, "rows")     ? 0
@@ -1032,16 +1034,18 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     k_pnn_work<a, b><<<work_ctas, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,\
                                                      gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
                                                      v->work_cap)
+            // k_pnn_lin's flush keeps byte offsets from the tile base in 32 bits: up to ~66
+            // planes of nx * ny voxels
             if (v->plane_lin && v->plane_walk && vec && tw == 4 && w % (4 * kChunk) == 0 &&
-                cal.probe != SVR_PROBE_FAN) {
-                const int nch = v->plane_lin == 2 ? 2 : 4;
+                cal.probe != SVR_PROBE_FAN && (long long)v->d.nx * v->d.ny * 8 * 72 < (1ll << 31)) {
+                const int nch = v->plane_lin == 2 ? 2 : v->plane_lin == 3 ? 8 : 4;
                 dim3 gl(ntx, m, (h + 32 * nch - 1) / (32 * nch));
 #define LL(bx_, n_)                                                                                \
     k_pnn_lin<bx_, n_><<<gl, 128, 0, v->stream>>>(p, pitch, fstride, h, fps + k0, v->d_fan, gd, v->acc, \
                                                   bx, stats, v->d_work, v->d_work_n, v->work_cap,  \
-                                                  1u << 20)
-                if (box) { if (nch == 4) LL(true, 4); else LL(true, 2); }
-                else { if (nch == 4) LL(false, 4); else LL(false, 2); }
+                                                  1u << 20, v->plane_flush_lin)
+                if (box) { if (nch == 4) LL(true, 4); else if (nch == 8) LL(true, 8); else LL(true, 2); }
+                else { if (nch == 4) LL(false, 4); else if (nch == 8) LL(false, 8); else LL(false, 2); }
 #undef LL
                 if (box)
                     k_pnn_work<true, true><<<work_ctas, 256, 0, v->stream>>>(
