@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspinevol_b200.so")
+# SVR_LIB_PATH: load another build of the library (A/B experiments with compile-time variants)
+LIB_PATH = os.environ.get("SVR_LIB_PATH") or os.path.join(_HERE, "libspinevol_b200.so")
 
 SVR_OK, SVR_E_INVALID, SVR_E_ALGO, SVR_E_IO, SVR_E_CUDA = 0, 2, 3, 4, 5
 PROBE_LINEAR, PROBE_FAN = 0, 1
