@@ -741,6 +741,10 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
             e = cudaMalloc(&v->tri, sizeof(float2) * v->nvox);
         }
     }
+    if (e == cudaSuccess) {  // the fill's reciprocal table (per device; idempotent)
+        k_init_rcp<<<1, kRecipN, 0, v->stream>>>();
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaMalloc(&v->d_stats, sizeof(ull) * kStCount);
     if (e == cudaSuccess) e = cudaMalloc(&v->d_counter, sizeof(ull) * 2);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i)
@@ -2026,7 +2030,8 @@ extern "C" int svr_selftest_value_rounding(int device, int64_t* mismatches) {
     unsigned long long* d = nullptr;
     CK(cudaMalloc(&d, sizeof(unsigned long long)));
     CK(cudaMemset(d, 0, sizeof(unsigned long long)));
-    k_selftest_value<<<255, 256>>>(d);
+    k_init_rcp<<<1, kRecipN>>>();
+    k_selftest_value<<<kRecipN - 1, 256>>>(d);
     k_selftest_div<<<1024, 256>>>(d);
     CKL();
     unsigned long long h = 0;
