@@ -1042,12 +1042,13 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             // planes of nx * ny voxels
             if (v->plane_lin && v->plane_walk && vec && tw == 4 && w % (4 * kChunk) == 0 &&
                 cal.probe != SVR_PROBE_FAN && (long long)v->d.nx * v->d.ny * 8 * 72 < (1ll << 31)) {
+                // SVR_PLANE_LIN: 1 = 64 x 128 px tiles (4 chunks per thread), 2 = 64 x 64, 3 = 64 x 256
                 const int nch = v->plane_lin == 2 ? 2 : v->plane_lin == 3 ? 8 : 4;
                 dim3 gl(ntx, m, (h + 32 * nch - 1) / (32 * nch));
-#define LL(bx_, n_)                                                                                \
-    k_pnn_lin<bx_, n_><<<gl, 128, 0, v->stream>>>(p, pitch, fstride, h, fps + k0, v->d_fan, gd, v->acc, \
-                                                  bx, stats, v->d_work, v->d_work_n, v->work_cap,  \
-                                                  1u << 20, v->plane_flush_lin)
+#define LL(bx_, n_)                                                                                 \
+    k_pnn_lin<bx_, n_, 4><<<gl, 128, 0, v->stream>>>(p, pitch, fstride, h, fps + k0, v->d_fan, gd, v->acc, \
+                                                     bx, stats, v->d_work, v->d_work_n, v->work_cap,  \
+                                                     1u << 20, v->plane_flush_lin)
                 if (box) { if (nch == 4) LL(true, 4); else if (nch == 8) LL(true, 8); else LL(true, 2); }
                 else { if (nch == 4) LL(false, 4); else if (nch == 8) LL(false, 8); else LL(false, 2); }
 #undef LL
