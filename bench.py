@@ -519,7 +519,7 @@ def run_ours(args):
                    "frames_this_rank": int(n_my)},
         "stages_ms": {"insert": ins_ms, "fill": fill_ms, "render": rend_ms},
         "insert_only": {"value": total_px / ins_s / 1e9 if world == 1 else None, "unit": UNIT},
-        "roofline": {"bound": "hbm", "kernel": "k_pnn_plane + k_pnn_work (K1)", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "k_pnn_lin + k_pnn_work (K1)", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,

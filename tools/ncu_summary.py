@@ -3,7 +3,7 @@
 launch, plus the DRAM traffic of the insert kernel (feeds bench.py's roofline.traffic).
 
   python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r1_ncu_full_summary.jsonl \
-      [--traffic profiles/insert_traffic.json --traffic-kernel k_pnn_plane]
+      [--traffic profiles/insert_traffic.json --traffic-kernel k_pnn_lin]
 """
 import argparse
 import csv
@@ -64,7 +64,7 @@ def main():
     ap.add_argument("report")
     ap.add_argument("out")
     ap.add_argument("--traffic")
-    ap.add_argument("--traffic-kernel", default="k_pnn_plane")
+    ap.add_argument("--traffic-kernel", default="k_pnn_lin")
     a = ap.parse_args()
     ds = list(rows(a.report))
     with open(a.out, "w") as f:
