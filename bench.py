@@ -235,6 +235,70 @@ def measure_config(name, steps=3):
     return out
 
 # ---------------------------------------------------------------- our arm
+def slab_shares(wl, frames, boxes, rp, stream, dev, ns=(2, 4, 8), steps=3, nlat=60):
+    """The N-GPU z-slab split replayed one slab at a time on this single GPU (no second GPU is
+    available to this build): for each N, the slab that receives the most frames gets its own
+    slab-sized VoxelGrid (owned + ghost planes) and runs (a) the batch step of its share (insert of
+    its routed frames, fill of its per-z-chunk boxes, render of its columns) and (b) the per-frame
+    incremental path (svr_frame_step) over frames from the middle of its share.  (a) is the N-GPU
+    step time before the gather of the coronal rows; (b) is the per-frame insert+render latency a
+    rank of an N-GPU run sees.  Nothing of another rank's work runs concurrently, so the GPU
+    timing is that rank's alone."""
+    import numpy as np
+    import torch
+
+    import paper_2412_00058_b200 as pkg
+    from paper_2412_00058_b200 import sharding, synth
+
+    fill_r = wl.fill_radius
+    ghost = fill_r + synth.CFG4_RENDER["median_radius"]
+    nz = wl.dims[2]
+    out = {}
+    for n in ns:
+        slabs = sharding.plan_slabs(nz, n, ghost)
+        routed = [sharding.route(boxes, sl.alloc) for sl in slabs]
+        r = max(range(n), key=lambda i: len(routed[i]))
+        sl, mine = slabs[r], routed[r]
+        g = pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, device=dev.index, z_range=sl.alloc)
+        g.set_stream(stream.cuda_stream)
+        fr = frames[torch.from_numpy(mine).to(dev)].contiguous()
+        po = wl.poses[mine]
+        fb = sharding.chunk_boxes(boxes, mine, sl.alloc, chunk=32, dilate=fill_r)
+        rb = sharding.chunk_boxes(boxes, mine, sl.alloc, chunk=32)
+        with torch.cuda.stream(stream):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            for i in range(steps + 2):
+                if i == 2:
+                    ev[0].record(stream)
+                g.insert_frames(fr, po, wl.calib)
+                g.fill_holes_boxes(fb, fill_r, pkg.FILL_MEAN, count=False)
+                g.render_coronal_boxes(rb, rp, fill_r)
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            step_ms = ev[0].elapsed_time(ev[1]) / steps
+            g.clear()
+            k0 = max(0, len(mine) // 2 - nlat // 2)
+            lat = []
+            for j in range(-3, min(nlat, len(mine) - k0)):
+                k = k0 + max(j, 0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g.frame_step(fr[k], po[k:k + 1], wl.calib, fill_r, rp)
+                b.record(stream)
+                stream.synchronize()
+                if j >= 0:
+                    lat.append(a.elapsed_time(b))
+        g.close()
+        del fr
+        lat.sort()
+        out[str(n)] = {"slab": r, "planes_stored": sl.alloc[1] - sl.alloc[0],
+                       "frames": int(len(mine)), "step_ms": step_ms,
+                       "step_gpx_s_job": wl.nframes * wl.w * wl.h / (step_ms / 1e3) / 1e9,
+                       "frame_p50_ms": lat[len(lat) // 2] if lat else None,
+                       "frame_p95_ms": lat[int(0.95 * (len(lat) - 1) + 0.5)] if lat else None}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -472,6 +536,14 @@ def run_ours(args):
                          "%d threads, %s" % (len(idx), args.cpu_every, px / 1e6, len(times), nth,
                                              _cpu_model())}
 
+    shares = None
+    if rank == 0 and world == 1 and not args.no_slab_shares:
+        shares = {"what": "N-GPU z-slab split replayed one slab at a time on this GPU: the busiest "
+                          "slab's batch step (before the coronal-row gather) and its per-frame "
+                          "latency (svr_frame_step p50/p95); step_gpx_s_job = whole-job pixels / "
+                          "that slab's step time",
+                  "n": slab_shares(wl, frames, boxes, rp, stream, dev)}
+
     others = None
     if rank == 0 and world == 1 and not args.no_other_configs:
         grid.close()
@@ -545,6 +617,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "exact_fallbacks_per_frame": stats["exact_fallbacks"] / max(stats["frames_inserted"], 1),
         "other_configs": others,
+        "slab_shares": shares,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -567,6 +640,7 @@ def main():
     ap.add_argument("--latency-frames", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true", help="skip cfg1/cfg3/cfg5 lines")
+    ap.add_argument("--no-slab-shares", action="store_true", help="skip the N = 2/4/8 slab-share replay")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N>1: gather the coronal strips with NCCL instead of the fused peer stores")
     ap.add_argument("--fused-gather-1", action="store_true",

@@ -742,7 +742,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         }
     }
     if (e == cudaSuccess) {  // the fill's reciprocal table (per device; idempotent)
-        k_init_rcp<<<1, kRecipN, 0, v->stream>>>();
+        k_init_rcp<<<1, 256, 0, v->stream>>>();
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMalloc(&v->d_stats, sizeof(ull) * kStCount);
@@ -2031,7 +2031,7 @@ extern "C" int svr_selftest_value_rounding(int device, int64_t* mismatches) {
     unsigned long long* d = nullptr;
     CK(cudaMalloc(&d, sizeof(unsigned long long)));
     CK(cudaMemset(d, 0, sizeof(unsigned long long)));
-    k_init_rcp<<<1, kRecipN>>>();
+    k_init_rcp<<<1, 256>>>();
     k_selftest_value<<<kRecipN - 1, 256>>>(d);
     k_selftest_div<<<1024, 256>>>(d);
     CKL();
