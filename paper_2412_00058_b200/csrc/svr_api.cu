@@ -145,7 +145,8 @@ struct svr_volume {
     int plane_lin = 1;          // SVR_PLANE_LIN: k_pnn_lin for linear probes (1: 128-row tiles, 2: 64), 0 k_pnn_plane
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
-    int fill_zc = 32;           // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32)
+    int num_sms = 148;          // the device's SM count (grid sizing)
+    int fill_zc = 0;            // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32; 0 = by region size)
     int fill_mode = SVR_FILL_MEAN;  // mode of the latest fill_holes: decodes the fill layer on readout
     bool fill_tma = false;      // SVR_FILL_KERNEL=tma selects k_fill_tma (opt-in: 0.43 vs 0.385 ms)
     int fill_tma_zc = 32;       // SVR_FILL_TMA_ZC: planes per CTA in k_fill_tma (16/32)
@@ -725,6 +726,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         return code;
     };
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(SVR_E_CUDA, "cudaSetDevice failed"));
+    cudaDeviceGetAttribute(&v->num_sms, cudaDevAttrMultiProcessorCount, device);
     v->nvox = (long long)desc->nx * desc->ny * (desc->z_end - desc->z_begin);
     const long long ncol = (long long)desc->nx * (desc->z_end - desc->z_begin);
     cudaError_t e = cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking);
@@ -1362,17 +1364,29 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         return SVR_OK;
     }
     if (mode == SVR_FILL_MEAN && radius == 1 && !v->fill_smem) {
-        const int zc = v->fill_zc;
         std::vector<BoxTiles> bt;
         long long total = 0;
-        for (const Box& b : bs) {
-            BoxTiles t;
-            t.b = b;
-            t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of fill_ty rows
-            t.nty = (b.y1 - b.y0 + 1 + 4 * v->fill_ty - 1) / (4 * v->fill_ty);
-            t.first = total;
-            total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
-            bt.push_back(t);
+        auto tile = [&](int zc) {
+            bt.clear();
+            total = 0;
+            for (const Box& b : bs) {
+                BoxTiles t;
+                t.b = b;
+                t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of fill_ty rows
+                t.nty = (b.y1 - b.y0 + 1 + 4 * v->fill_ty - 1) / (4 * v->fill_ty);
+                t.first = total;
+                total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
+                bt.push_back(t);
+            }
+        };
+        // planes per march: SVR_FILL_ZC, else 32 unless that leaves fewer than ~8 CTAs per SM
+        // (a slab's share of a multi-GPU split, small incremental boxes): then 16 or 8
+        int zc = v->fill_zc > 0 ? v->fill_zc : 32;
+        tile(zc);
+        const long long want = 8ll * v->num_sms;
+        while (v->fill_zc <= 0 && v->fill_depth != 2 && v->fill_ty == 8 && zc > 8 && total < want) {
+            zc /= 2;
+            tile(zc);
         }
         void* d = nullptr;
         if (int e = upload_tiles(v, bt.data(), sizeof(BoxTiles) * bt.size(), &d)) return e;
@@ -1392,9 +1406,11 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         } else if (ty == 16) {
             FW(16, 1, 16);
         } else {
-            if (zc == 8) FW(8, 1, 8);
-            else if (zc == 32 && !count)
-                k_fill_warp<32, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
+            if (!count) {
+                if (zc == 8) k_fill_warp<8, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
+                else if (zc == 32) k_fill_warp<32, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
+                else k_fill_warp<16, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
+            } else if (zc == 8) FW(8, 1, 8);
             else if (zc == 32) FW(32, 1, 8);
             else FW(16, 1, 8);
         }
