@@ -398,7 +398,7 @@ def run_ours(args):
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.warmup + args.steps)]
 
-    def step(i):
+    def step_seq(i):  # insert all, fill all, render all: the stage breakdown
         e = ev[i]
         e[0].record(stream)
         grid.insert_frames(frames, poses, wl.calib)
@@ -407,6 +407,21 @@ def run_ours(args):
         e[2].record(stream)
         grid.render_coronal_boxes(render_boxes, rp, fill_r)
         e[3].record(stream)
+        gather()
+
+    # --sweep-groups > 1: the same work with the fill / render of every finished z-chunk on a
+    # second (high-priority) stream while later frames are inserted (sharding.reconstruct_sweep;
+    # identical results, tests/test_gpu_parity.py::test_reconstruct_sweep_equals_sequential)
+    sched = sharding.sweep_schedule(boxes, mine, fill_boxes, render_boxes, groups=args.sweep_groups)
+    aux = torch.cuda.Stream(device=dev, priority=-1)
+    sweep_ev = [torch.cuda.Event() for _ in sched]
+
+    def step(i):
+        if args.sweep_groups <= 1:
+            step_seq(i)
+            return
+        sharding.reconstruct_sweep(grid, frames, poses, wl.calib, sched, rp, fill_r,
+                                   insert_stream=stream, aux_stream=aux, events=sweep_ev)
         gather()
 
     with torch.cuda.stream(stream):
@@ -444,10 +459,18 @@ def run_ours(args):
         barrier()
         launches = grid.stats()["kernel_launches"] - launches0
         elapsed_ms = allmax(t0.elapsed_time(t1))
-        timed = ev[args.warmup:]
-        ins_ms = allmax(sum(e[0].elapsed_time(e[1]) for e in timed) / args.steps)
-        fill_ms = allmax(sum(e[1].elapsed_time(e[2]) for e in timed) / args.steps)
-        rend_ms = allmax(sum(e[2].elapsed_time(e[3]) for e in timed) / args.steps)
+        # stage breakdown (and K1's time for the roofline) from the sequential schedule
+        ns = 3
+        step_seq(0)  # untimed: the first whole-batch insert after group inserts regrows buffers
+        torch.cuda.synchronize()
+        for i in range(ns):
+            step_seq(i)
+        torch.cuda.synchronize()
+        timed = ev[:ns]
+        ins_ms = allmax(sum(e[0].elapsed_time(e[1]) for e in timed) / ns)
+        fill_ms = allmax(sum(e[1].elapsed_time(e[2]) for e in timed) / ns)
+        rend_ms = allmax(sum(e[2].elapsed_time(e[3]) for e in timed) / ns)
+        seq_ms = allmax(sum(e[0].elapsed_time(e[3]) for e in timed) / ns)
 
         # ---- e2e through the public API from pinned host frames
         frames_host = frames.cpu().pin_memory()
@@ -589,7 +612,9 @@ def run_ours(args):
                    "gather": gather_mode if world > 1 or fused_try else None, "gather_note": gather_note or None,
                    "l2": "no flush: frames (590 MB) and volume (2.1 GB) exceed the 126 MB L2",
                    "frames_this_rank": int(n_my)},
-        "stages_ms": {"insert": ins_ms, "fill": fill_ms, "render": rend_ms},
+        "stages_ms": {"insert": ins_ms, "fill": fill_ms, "render": rend_ms, "sequential_step": seq_ms,
+                      "what": "insert-all / fill-all / render-all schedule, CUDA events per stage "
+                              "(timed step: %d frame group(s))" % args.sweep_groups},
         "insert_only": {"value": total_px / ins_s / 1e9 if world == 1 else None, "unit": UNIT},
         "roofline": {"bound": "hbm", "kernel": "k_pnn_lin + k_pnn_work (K1)", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
@@ -641,6 +666,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true", help="skip cfg1/cfg3/cfg5 lines")
     ap.add_argument("--no-slab-shares", action="store_true", help="skip the N = 2/4/8 slab-share replay")
+    ap.add_argument("--sweep-groups", type=int, default=1,
+                    help="frame groups of the overlapped insert / fill / render schedule (1 = sequential; "
+                         "4 / 8 measured slower: K1 is issue-bound, the overlap only adds launches)")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N>1: gather the coronal strips with NCCL instead of the fused peer stores")
     ap.add_argument("--fused-gather-1", action="store_true",

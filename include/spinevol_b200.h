@@ -146,6 +146,9 @@ int svr_create(const svr_grid_desc* desc, int device, svr_volume** out);
 int svr_destroy(svr_volume* vol);
 /* Use an external cudaStream_t (e.g. the caller's) for every later call. NULL = own stream. */
 int svr_set_stream(svr_volume* vol, void* cuda_stream);
+/* Switch to an external stream WITHOUT synchronizing the current one: the caller orders the two
+ * streams (events).  Used to overlap fill / render of finished z-chunks with later inserts. */
+int svr_use_stream(svr_volume* vol, void* cuda_stream);
 /* zero accumulators, fill layer, render images, stats */
 int svr_clear(svr_volume* vol);
 int svr_sync(svr_volume* vol);

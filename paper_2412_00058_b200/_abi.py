@@ -100,6 +100,7 @@ SIGNATURES = {
     "svr_create": (C.c_int, [PG, C.c_int, C.POINTER(P)]),
     "svr_destroy": (C.c_int, [P]),
     "svr_set_stream": (C.c_int, [P, P]),
+    "svr_use_stream": (C.c_int, [P, P]),
     "svr_clear": (C.c_int, [P]),
     "svr_sync": (C.c_int, [P]),
     "svr_get_desc": (C.c_int, [P, PG]),

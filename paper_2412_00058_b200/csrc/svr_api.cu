@@ -93,6 +93,7 @@ struct svr_volume {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = true;
+    cudaStream_t own_stream_saved = nullptr;  // the handle's own stream while svr_use_stream lends another
     cudaStream_t copy_stream = nullptr;
     long long nvox = 0;
     ull* acc = nullptr;
@@ -132,7 +133,15 @@ struct svr_volume {
     FrameGraph fg;                  // svr_frame_step graph
     GatherTargets gt{nullptr, 0, 0, 0, 0};  // fused render + gather targets (device pointer array)
     float** d_gt = nullptr;
-    void* d_tiles = nullptr;        // region tables of the multi-box fill / render launches
+    // region tables of the multi-box fill / render launches: a ring of pinned staging + device
+    // slots, so an upload never blocks the host behind queued work (a pageable copy would: it
+    // serialised the overlapped sweep's host thread with the fill / render stream)
+    static constexpr int kTileSlots = 4;
+    void* d_tiles[kTileSlots] = {};
+    void* h_tiles[kTileSlots] = {};
+    cudaEvent_t tiles_ev[kTileSlots] = {};
+    int tiles_prev = -1;
+    cudaStream_t tiles_prev_stream = nullptr;
     size_t tiles_cap = 0;
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
@@ -657,7 +666,11 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
     cudaFree(v->d_work);
-    cudaFree(v->d_tiles);
+    for (int i = 0; i < svr_volume::kTileSlots; ++i) {
+        cudaFree(v->d_tiles[i]);
+        cudaFreeHost(v->h_tiles[i]);
+        if (v->tiles_ev[i]) cudaEventDestroy(v->tiles_ev[i]);
+    }
     cudaFree(v->d_work_n);
     cudaFree(v->d_gt);
     if (v->fg.exec) cudaGraphExecDestroy(v->fg.exec);
@@ -679,6 +692,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     for (int i = 0; i < 2; ++i)
         if (v->params_ev[i]) cudaEventDestroy(v->params_ev[i]);
     if (v->own_stream && v->stream) cudaStreamDestroy(v->stream);
+    if (v->own_stream_saved) cudaStreamDestroy(v->own_stream_saved);
     if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
     cudaGetLastError();
     delete v;
@@ -777,10 +791,25 @@ extern "C" int svr_set_stream(svr_volume* v, void* s) {
     if (s) {
         v->stream = (cudaStream_t)s;
         v->own_stream = false;
+    } else if (v->own_stream_saved) {
+        v->stream = v->own_stream_saved;
+        v->own_stream_saved = nullptr;
+        v->own_stream = true;
     } else {
         CK(cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking));
         v->own_stream = true;
     }
+    return SVR_OK;
+}
+
+extern "C" int svr_use_stream(svr_volume* v, void* s) {
+    VOL_CHECK(v);
+    if (!s) return fail(SVR_E_INVALID, "svr_use_stream needs a stream");
+    if (v->own_stream && v->stream) {  // the handle's own stream stays alive for later calls
+        v->own_stream_saved = v->stream;
+        v->own_stream = false;
+    }
+    v->stream = (cudaStream_t)s;
     return SVR_OK;
 }
 
@@ -1284,16 +1313,33 @@ static bool clip_box(const svr_volume* v, const svr_box* in, Box* out) {
 // Upload a small region table to the handle's device scratch (stream-ordered: the copy runs after
 // every earlier kernel of the stream, so one buffer serves consecutive launches).
 static int upload_tiles(svr_volume* v, const void* host, size_t bytes, void** dev) {
+    constexpr int K = svr_volume::kTileSlots;
+    if (!v->tiles_ev[0])
+        for (int i = 0; i < K; ++i) CK(cudaEventCreateWithFlags(&v->tiles_ev[i], cudaEventDisableTiming));
+    // the previous slot's consumers were enqueued on its stream since its upload: mark them
+    if (v->tiles_prev >= 0) CK(cudaEventRecord(v->tiles_ev[v->tiles_prev], v->tiles_prev_stream));
+    const int s = (v->tiles_prev + 1) % K;
+    CK(cudaEventSynchronize(v->tiles_ev[s]));  // this slot's last consumers (K uploads ago) are done
     if (bytes > v->tiles_cap) {
-        CK(cudaStreamSynchronize(v->stream));
-        cudaFree(v->d_tiles);
-        v->d_tiles = nullptr;
+        CK(cudaDeviceSynchronize());
+        const size_t cap = std::max<size_t>(bytes, 4096);
+        for (int i = 0; i < K; ++i) {
+            cudaFree(v->d_tiles[i]);
+            cudaFreeHost(v->h_tiles[i]);
+            v->d_tiles[i] = v->h_tiles[i] = nullptr;
+        }
         v->tiles_cap = 0;
-        CK(cudaMalloc(&v->d_tiles, std::max<size_t>(bytes, 4096)));
-        v->tiles_cap = std::max<size_t>(bytes, 4096);
+        for (int i = 0; i < K; ++i) {
+            CK(cudaMalloc(&v->d_tiles[i], cap));
+            CK(cudaMallocHost(&v->h_tiles[i], cap));
+        }
+        v->tiles_cap = cap;
     }
-    CK(cudaMemcpyAsync(v->d_tiles, host, bytes, cudaMemcpyHostToDevice, v->stream));
-    *dev = v->d_tiles;
+    std::memcpy(v->h_tiles[s], host, bytes);
+    CK(cudaMemcpyAsync(v->d_tiles[s], v->h_tiles[s], bytes, cudaMemcpyHostToDevice, v->stream));
+    v->tiles_prev = s;
+    v->tiles_prev_stream = v->stream;
+    *dev = v->d_tiles[s];
     return SVR_OK;
 }
 

@@ -98,7 +98,12 @@ class VoxelGrid:
     def slab(self):
         return (self.desc.z_begin, self.desc.z_end)
 
-    def set_stream(self, cuda_stream: int | None):
+    def set_stream(self, cuda_stream: int | None, sync: bool = True):
+        """Run later calls on `cuda_stream` (None: the handle's own).  sync=False switches without
+        synchronizing the current stream (svr_use_stream): the caller orders the streams."""
+        if not sync:
+            check(lib().svr_use_stream(self._h, C.c_void_p(cuda_stream)))
+            return
         check(lib().svr_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
 
     def clear(self):

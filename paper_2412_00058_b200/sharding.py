@@ -101,3 +101,73 @@ def chunk_boxes(boxes, idx, alloc, chunk: int = 32, dilate: int = 0):
         out.append(_abi.Box(min(b.x0 for b in sel) - d, min(b.y0 for b in sel) - d, z0,
                             max(b.x1 for b in sel) + d, max(b.y1 for b in sel) + d, z1))
     return out
+
+
+def sweep_schedule(boxes, idx, fill_boxes, render_boxes, groups: int = 8, margin: int = 8):
+    """Plan a batch reconstruction whose hole fill and render of finished z-chunks overlap the
+    inserts of later frames (see `reconstruct_sweep`).  The frames `idx` (in sweep order) are cut
+    into `groups` contiguous groups; a chunk box is ready once every frame whose conservative box
+    meets its planes widened by `margin` (>= fill radius + the render's median and band reach) has
+    been inserted.  Returns [(frame_begin, frame_end, fill_boxes_ready, render_boxes_ready)] with
+    positions into `idx`; every box appears exactly once, in z order."""
+    n = len(idx)
+    groups = max(1, min(groups, n))
+    cuts = [round(n * g / groups) for g in range(groups + 1)]
+
+    def ready(b):  # position after the last frame that meets the widened chunk
+        last = 0
+        for p, k in enumerate(idx):
+            fb = boxes[int(k)]
+            if not fb.empty() and fb.z1 >= b.z0 - margin and fb.z0 <= b.z1 + margin:
+                last = p + 1
+        return last
+
+    def group_of(b):
+        r = ready(b)
+        for g in range(groups):
+            if r <= cuts[g + 1]:
+                return g
+        return groups - 1
+
+    fg = [group_of(b) for b in fill_boxes]
+    rg = [group_of(b) for b in render_boxes]
+    # a chunk's render reads its own and its neighbours' fill layer: never ahead of the fills
+    for i, b in enumerate(render_boxes):
+        for j, fb_ in enumerate(fill_boxes):
+            if fb_.z1 >= b.z0 - margin and fb_.z0 <= b.z1 + margin:
+                rg[i] = max(rg[i], fg[j])
+    out = []
+    for g in range(groups):
+        out.append((cuts[g], cuts[g + 1], [b for b, x in zip(fill_boxes, fg) if x == g],
+                    [b for b, x in zip(render_boxes, rg) if x == g]))
+    return out
+
+
+def reconstruct_sweep(grid, frames, poses, calib, schedule, render_params, fill_radius: int = 1,
+                      insert_stream=None, aux_stream=None, events=None):
+    """Insert + mean fill + depth-band render of a batch, with the fill / render of every finished
+    z-chunk (`sweep_schedule`) running on `aux_stream` while later frames are inserted on
+    `insert_stream` (torch streams; default: the current stream and a new one).  The result is
+    identical to insert-all, fill-all, render-all: each chunk is filled and rendered only after
+    every frame that can reach it, chunks are processed in z order on one stream, and a column's
+    last depth / band write is the one made after its neighbours' fills.  On return the insert
+    stream has waited for the aux stream."""
+    import torch
+
+    s_ins = insert_stream or torch.cuda.current_stream()
+    s_aux = aux_stream or torch.cuda.Stream(device=s_ins.device)
+    evs = events or [torch.cuda.Event() for _ in schedule]
+    for (a, b, fb, rb), ev in zip(schedule, evs):
+        grid.set_stream(s_ins.cuda_stream, sync=False)
+        if b > a:
+            grid.insert_frames(frames[a:b], poses[a:b], calib)
+        if fb or rb:
+            ev.record(s_ins)
+            s_aux.wait_event(ev)
+            grid.set_stream(s_aux.cuda_stream, sync=False)
+            if fb:
+                grid.fill_holes_boxes(fb, fill_radius, _abi.FILL_MEAN, count=False)
+            if rb:
+                grid.render_coronal_boxes(rb, render_params, fill_radius)
+    s_ins.wait_stream(s_aux)
+    grid.set_stream(s_ins.cuda_stream, sync=False)

@@ -646,3 +646,44 @@ def test_checkpoint_resume(tmp_path):
     other = pkg.VoxelGrid((8, 8, 8), 1.0, (0, 0, 0), device=0)
     with pytest.raises(pkg.InvalidInput):
         other.load(tmp_path / "ck.npz")
+
+
+@pytest.mark.parametrize("groups", [3, 8])
+def test_reconstruct_sweep_equals_sequential(groups):
+    """sharding.reconstruct_sweep (fill / render of finished z-chunks on a second stream while
+    later frames are inserted) leaves the accumulators, the fill layer and the coronal images bit
+    for bit as insert-all, fill-all, render-all does."""
+    import torch
+    from paper_2412_00058_b200 import sharding
+    wl = synth.cfg2(nframes=600)
+    frames = torch.empty((600, wl.h, wl.w), dtype=torch.uint8, device="cuda")
+    synth.synth_frames_device(wl, frames, 0, 600, 0)
+    rp = synth.render_params()
+    fill_r = wl.fill_radius
+    alloc = (0, wl.dims[2])
+    idx = np.arange(600)
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    fb = sharding.chunk_boxes(boxes, idx, alloc, chunk=32, dilate=fill_r)
+    rb = sharding.chunk_boxes(boxes, idx, alloc, chunk=32)
+
+    seq = _grid(wl)
+    seq.insert_frames(frames, wl.poses[:600], wl.calib)
+    seq.fill_holes_boxes(fb, fill_r, pkg.FILL_MEAN, count=False)
+    seq.render_coronal_boxes(rb, rp, fill_r)
+    seq.sync()
+
+    sched = sharding.sweep_schedule(boxes, idx, fb, rb, groups=groups)
+    assert sum(len(s[2]) for s in sched) == len(fb) and sum(len(s[3]) for s in sched) == len(rb)
+    assert sum(len(s[3]) for s in sched[:-1]) > 0, "nothing overlapped"
+    pip = _grid(wl)
+    s_ins = torch.cuda.Stream()
+    with torch.cuda.stream(s_ins):
+        sharding.reconstruct_sweep(pip, frames, wl.poses[:600], wl.calib, sched, rp, fill_r,
+                                   insert_stream=s_ins)
+    s_ins.synchronize()
+    pip.sync()
+    for a, b in zip(seq.accumulators(), pip.accumulators()):
+        assert np.array_equal(a, b)
+    assert np.array_equal(seq.fill_layer(), pip.fill_layer())
+    for a, b in zip(seq.read_coronal(), pip.read_coronal()):
+        assert np.array_equal(a, b)
