@@ -334,6 +334,11 @@ static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, doubl
         for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = a.Mv[3 * k + j];
     }
     if (!ok) return fail(SVR_E_INVALID, "pose maps the frame too far from the grid (|u| >= 1e8 voxels)");
+    for (int k = 0; k < 3; ++k) {  // k_pnn_lin tile corners: 64 columns x 128 rows
+        const long long c1 = 63ll * fp->Dc[k], r1 = 127ll * fp->Dr[k];
+        fp->tmn[k] = std::min(std::min(0ll, c1), std::min(r1, c1 + r1));
+        fp->tmx[k] = std::max(std::max(0ll, c1), std::max(r1, c1 + r1));
+    }
     fp->pose = pose;
     fp->cal = x.cal;
     fp->g = x.g;
