@@ -151,6 +151,7 @@ struct svr_volume {
     int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
     int plane_tw_cur = 4;       // the width chosen for the current insert call
     int plane_flush_lin = 1;    // SVR_PLANE_FLUSH: k_pnn_lin table flush, 1 linear over all threads, 0 lane = x
+    int lin_small = 4;          // SVR_LIN_SMALL: launches of <= this many frames use 64-row k_pnn_lin tiles
     int plane_lin = 1;          // SVR_PLANE_LIN: k_pnn_lin for linear probes (1: 128-row tiles, 2: 64), 0 k_pnn_plane
     int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
     bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
@@ -731,6 +732,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     }
     if (const char* e = std::getenv("SVR_PLANE_TW")) v->plane_tw = std::atoi(e) == 6 ? 6 : 4;
     if (const char* e = std::getenv("SVR_PLANE_FLUSH")) v->plane_flush_lin = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("SVR_LIN_SMALL")) v->lin_small = std::atoi(e);
     if (const char* e = std::getenv("SVR_PLANE_LIN")) v->plane_lin = std::min(3, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
@@ -1079,7 +1081,10 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             if (v->plane_lin && v->plane_walk && vec && tw == 4 && w % (4 * kChunk) == 0 &&
                 cal.probe != SVR_PROBE_FAN && (long long)v->d.nx * v->d.ny * 8 * 72 < (1ll << 31)) {
                 // SVR_PLANE_LIN: 1 = 64 x 128 px tiles (4 chunks per thread), 2 = 64 x 64, 3 = 64 x 256
-                const int nch = v->plane_lin == 2 ? 2 : v->plane_lin == 3 ? 8 : 4;
+                // a launch of a few frames (the per-frame path) takes 64-row tiles: twice the CTAs,
+                // half the pixels on each one's critical path
+                const int nch = (v->plane_lin == 2 || (v->plane_lin == 1 && m <= v->lin_small)) ? 2
+                                : v->plane_lin == 3 ? 8 : 4;
                 dim3 gl(ntx, m, (h + 32 * nch - 1) / (32 * nch));
 #define LL(bx_, n_)                                                                                 \
     k_pnn_lin<bx_, n_, 4><<<gl, 128, 0, v->stream>>>(p, pitch, fstride, h, fps + k0, v->d_fan, gd, v->acc, \
