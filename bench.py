@@ -459,14 +459,19 @@ def run_ours(args):
         barrier()
         launches = grid.stats()["kernel_launches"] - launches0
         elapsed_ms = allmax(t0.elapsed_time(t1))
-        # stage breakdown (and K1's time for the roofline) from the sequential schedule
-        ns = 3
-        step_seq(0)  # untimed: the first whole-batch insert after group inserts regrows buffers
-        torch.cuda.synchronize()
-        for i in range(ns):
-            step_seq(i)
-        torch.cuda.synchronize()
-        timed = ev[:ns]
+        # stage breakdown (and K1's time for the roofline) from the sequential schedule: the timed
+        # steps' own events, or (overlapped sweep) a few extra sequential steps
+        if args.sweep_groups <= 1:
+            ns = args.steps
+            timed = ev[args.warmup:args.warmup + ns]
+        else:
+            ns = 3
+            step_seq(0)  # untimed: the first whole-batch insert after group inserts regrows buffers
+            torch.cuda.synchronize()
+            for i in range(ns):
+                step_seq(i)
+            torch.cuda.synchronize()
+            timed = ev[:ns]
         ins_ms = allmax(sum(e[0].elapsed_time(e[1]) for e in timed) / ns)
         fill_ms = allmax(sum(e[1].elapsed_time(e[2]) for e in timed) / ns)
         rend_ms = allmax(sum(e[2].elapsed_time(e[3]) for e in timed) / ns)
