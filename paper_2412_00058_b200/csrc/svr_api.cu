@@ -17,6 +17,7 @@
 
 #include "svr_host.hpp"
 #include "svr_kernels.cuh"
+#include "svr_k1.cuh"
 
 using namespace svr;
 
@@ -83,9 +84,10 @@ struct FrameGraph {
     unsigned char* d_tiles = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t frame_copy = nullptr;
     cudaEvent_t done = nullptr;
     int kernels = 0;
+    int shape = -1;        // k_pnn_tiles shape of the captured insert (-1: none)
+    uint64_t captures = 0; // graph (re-)captures so far
 };
 
 struct svr_volume {
@@ -150,6 +152,8 @@ struct svr_volume {
     int depth_seg = 4;          // SVR_DEPTH_SEG: threads per column in k_depth (4; 8 or 1 A/B)
     int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
     int plane_tw_cur = 4;       // the width chosen for the current insert call
+    int lin_shapes_cur = 0;     // k_pnn_tiles shapes every frame of the current insert call fits
+    int tiles_occ[8] = {};      // k_pnn_tiles resident CTAs per SM, per <shape, box> (lazy)
     int plane_flush_lin = 1;    // SVR_PLANE_FLUSH: k_pnn_lin table flush, 1 linear over all threads, 0 lane = x
     int lin_small = 4;          // SVR_LIN_SMALL: launches of <= this many frames use 64-row k_pnn_lin tiles
     int plane_lin = 1;          // SVR_PLANE_LIN: k_pnn_lin for linear probes (1: 128-row tiles, 2: 64), 0 k_pnn_plane
@@ -281,7 +285,31 @@ struct PrepCtx {
     double coef_bound; // coefficient rounding part of the tie bound, voxels
     DevCalib cal;
     GridDev g;
+    bool lin_ok;       // k_pnn_tiles usable at all (linear probe, grid planes addressable)
+    int lin_count_ok;  // tile shapes whose per-slot pixel count provably stays <= 4095
 };
+
+// k_pnn_tiles shapes (svr_k1.cuh): s = (NCH == 2) + 2 (NW == 2); columns 16 NCH x rows 32 NW
+static inline int shape_cols(int s) { return (s & 1) ? 32 : 64; }
+static inline int shape_rows(int s) { return (s & 2) ? 64 : 128; }
+
+// Bit s set when every tile of shape s of this frame keeps its voxel footprint inside the
+// shared table (X <= 32 columns, Y <= 62 rows: X = floor(max) - floor(min) + 1 <= floor(span) + 2)
+// and every step is below one voxel (one carry per axis and pixel).
+static int tile_shapes_fit(const long long Dc[3], const long long Dr[3], int count_ok) {
+    const double s = 1.0 / 4294967296.0;
+    int m = 0;
+    for (int k = 0; k < 3; ++k)
+        if (std::llabs(Dc[k]) >= (1ll << 32)) return 0;
+    for (int sh = 0; sh < 4; ++sh) {
+        if (!((count_ok >> sh) & 1)) continue;
+        const double c1 = shape_cols(sh) - 1, r1 = shape_rows(sh) - 1;
+        const double spx = (c1 * std::fabs((double)Dc[0]) + r1 * std::fabs((double)Dr[0])) * s;
+        const double spy = (c1 * std::fabs((double)Dc[1]) + r1 * std::fabs((double)Dr[1])) * s;
+        if (std::floor(spx + 1e-9) + 2 <= 32 && std::floor(spy + 1e-9) + 2 <= 62) m |= 1 << sh;
+    }
+    return m;
+}
 
 static double norm3(double a, double b, double c) { return std::sqrt(a * a + b * b + c * c); }
 
@@ -304,6 +332,27 @@ static PrepCtx prep_ctx(const svr_calib& c, const svr_grid_desc& g) {
     x.coef_bound = (std::ldexp(1.0, -33) + std::ldexp(1.0, -40)) * (double)(c.crop_w + c.crop_h + 1);
     x.cal = dev_calib(c);
     x.g = dev_grid(g);
+    // k_pnn_tiles: the flush addresses z planes by 32-bit byte offsets from the tile base (at most
+    // ~66 planes of nx * ny voxels); the table word packs count (12 bits) | sum (20 bits), so no
+    // voxel may collect more than 4095 pixels of one tile.  A voxel takes at most
+    // floor(1 / max_k |Dc_k|) + 1 pixels of a row and floor(1 / max_k |Dr_k|) + 1 of a column, and
+    // max_k |D_k| >= |D| / sqrt(3) = scale / (sqrt(3) voxel) for any pose (|q| = 1; the bound holds
+    // for the rotation part, so it is pose-independent and a captured frame graph stays valid).
+    x.lin_ok = c.probe == SVR_PROBE_LINEAR && (double)g.nx * g.ny * 8.0 * 70.0 < 4294967296.0;
+    x.lin_count_ok = 0;
+    if (x.lin_ok) {
+        const double q2 = c.image_to_transducer.qw * c.image_to_transducer.qw +
+                          c.image_to_transducer.qx * c.image_to_transducer.qx +
+                          c.image_to_transducer.qy * c.image_to_transducer.qy +
+                          c.image_to_transducer.qz * c.image_to_transducer.qz;
+        // non-unit quaternions scale the map by |q|^2: the calibration's is taken as it is, the
+        // pose's is required to be >= 0.98 per frame (make_params)
+        const double qs = std::min(1.0, q2) * 0.98;
+        const double nc = std::floor(std::sqrt(3.0) * g.voxel_mm / (c.scale_x_mm * qs)) + 1;
+        const double nr = std::floor(std::sqrt(3.0) * g.voxel_mm / (c.scale_y_mm * qs)) + 1;
+        for (int sh = 0; sh < 4; ++sh)
+            if (std::min(nc * shape_rows(sh), nr * shape_cols(sh)) <= 4095) x.lin_count_ok |= 1 << sh;
+    }
     return x;
 }
 
@@ -343,6 +392,7 @@ static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, doubl
     fp->pose = pose;
     fp->cal = x.cal;
     fp->g = x.g;
+    fp->lin_fit = 0;
     // Tie window: |fixed - real| <= coefficient rounding over 1 + col + row exact
     // integer steps, plus the deviation of an fp64 evaluation from real arithmetic -- the
     // reference chain's and this host map's (K) alike -- bounded by 512 roundings of the largest
@@ -376,6 +426,11 @@ static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, doubl
         } else {
             fp->pz[0] = fp->pz[1] = fp->pz[2] = fp->pz[3] = 0.0;
         }
+    }
+    {
+        const double qp2 = pose.qw * pose.qw + pose.qx * pose.qx + pose.qy * pose.qy + pose.qz * pose.qz;
+        if (fp->plane_ok && x.lin_ok && qp2 >= 0.98)  // (the count bound in prep_ctx assumes |q|^2 >= 0.98)
+            fp->lin_fit = tile_shapes_fit(fp->Dc, fp->Dr, x.lin_count_ok);
     }
     return SVR_OK;
 }
@@ -1028,6 +1083,60 @@ static void launch_rows_t(svr_volume* v, const uint8_t* px, long long pitch, lon
     v->launches++;
 }
 
+// K1 for linear probes: k_pnn_tiles (persistent over the launch's tiles) + the exact pass.
+template <int NCH, int NW, bool kBox>
+static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
+    const int slot = (NCH == 2) + 2 * (NW == 2) + 4 * kBox;
+    if (!v->tiles_occ[slot]) {
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pnn_tiles<NCH, NW, kBox>, 32 * NW, 0));
+        v->tiles_occ[slot] = std::max(1, occ);
+    }
+    const long long ctas = std::min<long long>(ta.ntiles, (long long)v->num_sms * v->tiles_occ[slot]);
+    k_pnn_tiles<NCH, NW, kBox><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
+    v->launches++;
+    return SVR_OK;
+}
+
+static int pick_shape(int shapes, int w, int nframes, int small) {
+    static const int big_pref[4] = {0, 1, 2, 3}, small_pref[4] = {1, 3, 0, 2};
+    const int* pref = nframes <= small ? small_pref : big_pref;
+    for (int i = 0; i < 4; ++i)
+        if (((shapes >> pref[i]) & 1) && w % shape_cols(pref[i]) == 0) return pref[i];
+    return -1;
+}
+
+static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, long long pitch,
+                        long long fstride, int w, int h, int m, const FrameParams* fps, int* boxes,
+                        ull* stats) {
+    TilesArgs ta;
+    ta.px = px;
+    ta.pitch = pitch;
+    ta.fstride = fstride;
+    ta.h = h;
+    ta.ntx = w / shape_cols(shape);
+    ta.nty = (h + shape_rows(shape) - 1) / shape_rows(shape);
+    ta.ntiles = (long long)m * ta.ntx * ta.nty;
+    ta.fps = fps;
+    ta.g = dev_grid(v->d);
+    ta.acc = v->acc;
+    ta.boxes = boxes;
+    ta.stats = stats;
+    ta.work = v->d_work;
+    ta.work_n = v->d_work_n;
+    ta.work_cap = v->work_cap;
+    switch (shape + 4 * box) {
+        case 0: return launch_tiles_t<4, 4, false>(v, ta);
+        case 1: return launch_tiles_t<2, 4, false>(v, ta);
+        case 2: return launch_tiles_t<4, 2, false>(v, ta);
+        case 3: return launch_tiles_t<2, 2, false>(v, ta);
+        case 4: return launch_tiles_t<4, 4, true>(v, ta);
+        case 5: return launch_tiles_t<2, 4, true>(v, ta);
+        case 6: return launch_tiles_t<4, 2, true>(v, ta);
+        default: return launch_tiles_t<2, 2, true>(v, ta);
+    }
+}
+
 // Launch over frames resident in device memory, chunked to the grid.y limit.
 //   PNN insert: k_pnn_plane + k_pnn_work (default, when tile_ok and no skip_zero), k_insert
 //   direct (SVR_INSERT_KERNEL=direct, skip_zero, narrow tiles), k_pnn_rows (=rows),
@@ -1043,11 +1152,42 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     const bool plane = mode == kModeInsert && v->insert_kernel == 3 && !skip && w >= 4 * kChunk &&
                        (long long)v->d.nx * v->d.ny < (1ll << 22) && tile_ok(v, cal, w, h, &ts, 4);
     const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
+    // k_pnn_tiles reads each row segment with 32-byte loads
+    const bool vec32 = ((uintptr_t)px % 32 == 0) && (pitch % 32 == 0) && (n == 1 || fstride % 32 == 0);
+    const int shape = (mode == kModeInsert && !skip && cal.probe == SVR_PROBE_LINEAR && vec32 &&
+                       v->insert_kernel == 3)
+                          ? pick_shape(v->lin_shapes_cur, w, n, v->lin_small)
+                          : -1;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
         const uint8_t* p = px + (long long)k0 * fstride;
         int* bx = boxes ? boxes + 6 * k0 : nullptr;
-        if (plane) {
+        if (shape >= 0) {
+            // k_pnn_tiles defers whole chunks with no overflow path: room for every chunk
+            const long long need = std::max<long long>(1ll << 20, (long long)m * h * (w / kChunk));
+            if (need > 0xffffffffll) return fail(SVR_E_INVALID, "insert batch too large");
+            if (!v->d_work || v->work_cap < need) {
+                CK(cudaStreamSynchronize(v->stream));
+                cudaFree(v->d_work);
+                v->d_work = nullptr;
+                v->work_cap = (unsigned int)need;
+                CK(cudaMalloc(&v->d_work, sizeof(ull) * v->work_cap));
+                if (!v->d_work_n) CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
+            }
+            CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
+            if (int e = launch_tiles(v, shape, box, p, pitch, fstride, w, h, m, fps + k0, bx, stats)) return e;
+            const int work_ctas = std::min(4096, std::max(16, 8 * m));
+            const GridDev gd = dev_grid(v->d);
+            if (box)
+                k_pnn_work<true, true><<<work_ctas, 256, 0, v->stream>>>(
+                    p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
+                    v->d_work_n, v->work_cap);
+            else
+                k_pnn_work<true, false><<<work_ctas, 256, 0, v->stream>>>(
+                    p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
+                    v->d_work_n, v->work_cap);
+            v->launches++;
+        } else if (plane) {
             const int cpr = (w + kChunk - 1) / kChunk;
             if (!v->d_work) {
                 v->work_cap = 1u << 20;
@@ -1181,6 +1321,8 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
     if (int e = ensure_fan(v, *c)) return e;
     // k_pnn_plane tile width: 6 chunks (96 px) when every frame's tile stays within the 32 x 32
     // voxel table (x extent over 96 columns + 64 rows, plus the +-1 margins), else 4
+    v->lin_shapes_cur = 0xf;
+    for (int k = 0; k < n; ++k) v->lin_shapes_cur &= hp[k].lin_fit;
     v->plane_tw_cur = 4;
     if (v->plane_tw == 6 && c->probe != SVR_PROBE_FAN) {
         double mx = 0.0, my = 0.0;
@@ -1210,7 +1352,7 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
                              want_box, boxes, mark, tag, stats);
     // host frames: double-buffered pinned staging, H2D on copy_stream overlapped with kernels
     const long long fb = (long long)w * h;                   // packed frame bytes
-    const long long pfb = (fb + 15) / 16 * 16;               // 16-B aligned frame stride
+    const long long pfb = (fb + 31) / 32 * 32;               // 32-B aligned frame stride
     const size_t want = (size_t)std::min<long long>(64ll << 20, pfb * n);
     if (int e = ensure_stage(v, std::max<size_t>(want, (size_t)pfb))) return e;
     const int per = (int)std::max<long long>(1, (long long)v->stage_bytes / pfb);
@@ -1991,7 +2133,6 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
     const DevCalib dc = dev_calib(c);
     const long long l0 = v->launches;
     CK(cudaStreamBeginCapture(v->stream, cudaStreamCaptureModeThreadLocal));
-    cudaMemcpyAsync(f.d_frame, f.h_frame, (size_t)w * h, cudaMemcpyDefault, v->stream);
     cudaMemcpyAsync(f.d_fp, f.h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, v->stream);
     cudaMemcpyAsync(f.d_tiles, f.h_tiles, kFgTileBytes, cudaMemcpyHostToDevice, v->stream);
     int e = insert_device(v, kModeInsert, f.d_frame, w, (long long)w * h, w, h, 1, f.d_fp, dc, false, false,
@@ -2019,21 +2160,6 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
     f.kernels = (int)(v->launches - l0) + 3;
     v->launches = l0;
     CK(cudaGraphInstantiate(&f.exec, f.graph, 0));
-    // the frame copy is the graph's memcpy node writing d_frame: its source is set per call
-    size_t nn = 0;
-    CK(cudaGraphGetNodes(f.graph, nullptr, &nn));
-    std::vector<cudaGraphNode_t> nodes(nn);
-    CK(cudaGraphGetNodes(f.graph, nodes.data(), &nn));
-    f.frame_copy = nullptr;
-    for (cudaGraphNode_t n : nodes) {
-        cudaGraphNodeType t;
-        CK(cudaGraphNodeGetType(n, &t));
-        if (t != cudaGraphNodeTypeMemcpy) continue;
-        cudaMemcpy3DParms mp;
-        CK(cudaGraphMemcpyNodeGetParams(n, &mp));
-        if (mp.dstPtr.ptr == f.d_frame) f.frame_copy = n;
-    }
-    if (!f.frame_copy) return fail(SVR_E_CUDA, "frame graph: frame copy node not found");
     f.w = w;
     f.h = h;
     f.fr = fr;
@@ -2075,20 +2201,36 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     const long long nf = (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 1) / 2);
     std::vector<ColTiles> cv{ct[0]}, mv{ct[1]};
     const long long nd = tile_cols(cv, 16), nm = tile_cols(mv);
-    if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm))
+    FrameParams fpar;
+    if (int e = make_params(*pose, prep_ctx(*c, v->d), c->scale_x_mm, c->scale_y_mm, &fpar)) return e;
+    // the insert's tile shape is part of the capture: a frame that fits none of the captured
+    // shape's tiles is still exact (its tiles take the exact pass) but re-captures once
+    const bool shape_ok = f.shape < 0 ? fpar.lin_fit == 0 : ((fpar.lin_fit >> f.shape) & 1) != 0;
+    if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm) || !shape_ok) {
+        v->lin_shapes_cur = fpar.lin_fit;
         if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;
-    if (int e = make_params(*pose, prep_ctx(*c, v->d), c->scale_x_mm, c->scale_y_mm, f.h_fp)) return e;
+        f.shape = pick_shape(fpar.lin_fit, w, 1, v->lin_small);
+        ++f.captures;
+    }
+    *f.h_fp = fpar;
     std::memcpy(f.h_tiles, &bt, sizeof bt);
     std::memcpy(f.h_tiles + sizeof(BoxTiles), &cv[0], sizeof(ColTiles));
     std::memcpy(f.h_tiles + sizeof(BoxTiles) + sizeof(ColTiles), &mv[0], sizeof(ColTiles));
     // frame source: device / pinned packed frames are copied straight from the caller
+    // (any row pitch: the node is a 2-D copy); pageable host frames are staged through pinned
+    // memory first, so the caller may reuse them on return
     bool pinned = false;
     const void* src = px;
-    if (!(is_device_ptr(px, &pinned) || pinned) || pitch != w) {
+    size_t spitch = (size_t)pitch;
+    if (!(is_device_ptr(px, &pinned) || pinned)) {
         for (int r = 0; r < h; ++r) std::memcpy(f.h_frame + (size_t)r * w, px + (size_t)r * pitch, (size_t)w);
         src = f.h_frame;
+        spitch = (size_t)w;
     }
-    CK(cudaGraphExecMemcpyNodeSetParams1D(f.exec, f.frame_copy, f.d_frame, src, (size_t)w * h, cudaMemcpyDefault));
+    // the frame copy is enqueued ahead of the graph (any pitch, any source memory): a graph
+    // memcpy node could not switch between host and device sources or pitches per call
+    CK(cudaMemcpy2DAsync(f.d_frame, (size_t)w, src, spitch, (size_t)w, (size_t)h, cudaMemcpyDefault,
+                         v->stream));
     CK(cudaGraphLaunch(f.exec, v->stream));
     CK(cudaEventRecord(f.done, v->stream));
     v->frames += 1;

@@ -1,0 +1,391 @@
+// svr_k1.cuh — K1, the pixel-nearest-neighbour insert of linear-probe B-scans,
+// as a persistent tile kernel.  Included by svr_api.cu after svr_kernels.cuh.
+//
+// Work unit: a tile of TCOLS = 16*NCH columns x TROWS = 32*NW rows of one frame.  Each CTA walks a
+// contiguous range of the launch's tiles (frame-major), so a frame's constants are loaded once per
+// ~30 tiles and the last wave is one tile long.
+//
+// Lane map: thread (warp w, lane l) walks the whole TCOLS-pixel row r = w + NW*l of the tile.  The
+// 32 lanes of a warp then sit on rows NW apart (cfg2: 1.67 voxels apart in y), so one shared
+// atomic of the warp hits ~2 banks' worth of words instead of ~4 (same-address lanes serialise
+// on B200: tools/ubench_atoms.cu; the bank model is in profiles/r2_opt_log.md).
+//
+// Per pixel the walk is, in SASS, 3 x (IADD3 with carry-out to a predicate + one predicated
+// address update) + a 3-input min (tie screen) + PRMT + ATOMS: the fixed-point fractions of
+// u = K + col*Dc + row*Dr (32.32) are stepped exactly, the index moves where a
+// fraction carries, and the shared-table byte address moves with it (x: +-4, y: +-4*STR,
+// z: XOR of the parity plane bit 1 << 13; a B-scan plane puts <= 2 z values in a voxel column).
+// A 16-pixel chunk whose fractions came within the certified tie window is undone and its
+// pixels go to the exact worklist pass (k_pnn_work), as before.
+//
+// Flush: the table's X x Y positions are spread linearly over all threads; each reads and
+// zeroes both parity slots (so the next tile starts from a clean table without a separate
+// zeroing pass), finds the slots' z from the frame plane and issues one predicated 64-bit
+// red.global.add per non-empty slot.
+#pragma once
+
+#ifndef SVR_TILES_PREFETCH
+#define SVR_TILES_PREFETCH 1  // k_pnn_tiles: L2 prefetch of each row's first voxel line
+#endif
+#ifndef SVR_TILES_MINB
+#define SVR_TILES_MINB 7  // k_pnn_tiles (128 threads): CTAs per SM the register budget is cut for
+#endif
+
+namespace svr {
+
+constexpr int kTabStr = 33;                    // table row stride in words (odd)
+constexpr int kTabPlane = 2048;                // words per parity plane: byte offset bit 13
+constexpr int kTabMaxY = kTabPlane / kTabStr;  // 62 voxel rows
+constexpr int kTabMaxX = 32;                   // voxel columns
+
+struct TilesArgs {
+    const uint8_t* px;
+    long long pitch, fstride;
+    int h;
+    int ntx, nty;        // tiles per frame
+    long long ntiles;    // nframes * ntx * nty
+    const FrameParams* fps;
+    GridDev g;
+    ull* acc;
+    int* boxes;
+    ull* stats;
+    ull* work;
+    unsigned int* work_n;
+    unsigned int work_cap;
+};
+
+// one exact step of the three fractions; the table byte address follows the carries
+__device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
+                                          uint32_t e0, uint32_t e1, uint32_t e2, uint32_t sx,
+                                          uint32_t sy) {
+    asm("{\n\t.reg .pred p0, p1, p2;\n\t.reg .u32 c0, c1, c2;\n\t"
+        "add.cc.u32 %0, %0, %4;\n\taddc.u32 c0, 0, 0;\n\t"
+        "add.cc.u32 %1, %1, %5;\n\taddc.u32 c1, 0, 0;\n\t"
+        "add.cc.u32 %2, %2, %6;\n\taddc.u32 c2, 0, 0;\n\t"
+        "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
+        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 xor.b32 %3, %3, 8192;\n\t}"
+        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a)
+        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy));
+}
+
+// A frame's constants, staged in shared memory when a CTA's tile range enters the frame (keeps
+// the 64-register budget for the walk).
+struct TileFrame {
+    long long A[3], Dc[3], Dr[3];  // 32.32 fixed: u(0,0) + 1/2, du/dcol, du/drow
+    long long cmn[3], cmx[3];      // min / max of (TCOLS - 1) Dc over {0, 1}
+    double pz[4];                  // frame plane (FrameParams::pz)
+    uint32_t E[3], neg[3];         // |Dc| low words; all-ones when Dc < 0 (mirrored fractions)
+    uint32_t te2, sx, sy;          // tie window + 1; table byte steps along x and y
+    int ok;                        // plane_ok and this tile shape fits (FrameParams::lin_fit)
+};
+
+__device__ __forceinline__ void push_work(const TilesArgs& ta, int f, int row, int cc) {
+    // the host sizes the list for every chunk of the launch, so it cannot overflow
+    const unsigned int slot = atomicAdd(ta.work_n, 1u);
+    ta.work[slot] = work_entry(f, row, cc, 0xffffu);
+}
+
+// Walk state (fractions + table byte address) of the pixel whose fixed-point u is (u0, u1, u2).
+// The index taken is the one the carries of W track: when lo + te2 wraps (the pixel sits in the
+// upper half of the tie window) the index is already one step further, so later pixels' indices
+// stay exact no matter where the row starts (the pixel itself is a tie and gets deferred).
+__device__ __forceinline__ void walk_state(long long u0, long long u1, long long u2, const TileFrame& fr,
+                                           int X0, int Y0, uint32_t& w0, uint32_t& w1, uint32_t& w2,
+                                           uint32_t& a) {
+    const uint32_t te2 = fr.te2;
+    const uint32_t m0 = (uint32_t)u0 ^ fr.neg[0], m1 = (uint32_t)u1 ^ fr.neg[1], m2 = (uint32_t)u2 ^ fr.neg[2];
+    w0 = m0 + te2;
+    w1 = m1 + te2;
+    w2 = m2 + te2;
+    // +-1 where the offset add wrapped (direction of the step: neg = all ones -> -1)
+    const int ix = (int)(u0 >> 32) + (w0 < te2 ? (fr.neg[0] ? -1 : 1) : 0);
+    const int iy = (int)(u1 >> 32) + (w1 < te2 ? (fr.neg[1] ? -1 : 1) : 0);
+    const int iz = (int)(u2 >> 32) + (w2 < te2 ? 1 : 0);  // (only the parity matters)
+    a = 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + ((uint32_t)(iz & 1) << 13);
+}
+
+// 32-byte row segment load (one LDG.256, L1 no-allocate: every byte is read once)
+__device__ __forceinline__ void ld256(const uint8_t* p, uint32_t* r) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "l"(p));
+}
+
+// unconditional 64-bit add of a table word (count << 20 | sum) as (count << 32 | sum)
+__device__ __forceinline__ void red_word(unsigned long long addr, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .b32 hi, lo;\n\t.reg .b64 w;\n\t"
+        "shr.u32 hi, %1, 20;\n\tand.b32 lo, %1, 1048575;\n\t"
+        "mov.b64 w, {lo, hi};\n\tred.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v) : "memory");
+}
+
+template <int NCH, int NW, bool kBox>
+__global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB) k_pnn_tiles(const TilesArgs ta) {
+    constexpr int NT = 32 * NW, TROWS = 32 * NW, TCOLS = 16 * NCH;
+    constexpr int kShape = (NCH == 2) + 2 * (NW == 2);
+    __shared__ __align__(16) uint32_t s_tab[2 * kTabPlane];
+    __shared__ TileFrame s_fr;
+    __shared__ unsigned int s_cnt[2];  // chunks counted out of bounds / deferred (rare: no registers)
+    __shared__ unsigned long long s_px;  // pixels of this CTA's tiles
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 2) s_cnt[tid] = 0u;
+    if (tid == 0) s_px = 0ull;
+    for (int i = tid; i < 2 * kTabPlane / 4; i += NT)
+        reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(s_tab);
+    const GridDev& g = ta.g;
+    const int tpf = ta.ntx * ta.nty;
+    const long long t0 = (long long)blockIdx.x * ta.ntiles / gridDim.x;
+    const long long t1 = (long long)(blockIdx.x + 1) * ta.ntiles / gridDim.x;
+    int f = (int)(t0 / tpf);
+    int rem = (int)(t0 - (long long)f * tpf);
+    int ty = rem / ta.ntx, tx = rem - ty * ta.ntx;
+    int cur_f = -1;
+    BoxAcc bb;
+
+    // Rows of a short last tile go to whole warps (rows w + S l, S = active warps): an idle warp
+    // skips the walk, and no idle lane's clamped address can collide with a live lane's bank.
+    auto tile_rows = [&](int tyq, int& S, int& row, bool& act, int& rowc) {
+        const int r0 = tyq * TROWS;
+        S = min(NW, (min(TROWS, ta.h - r0) + 31) >> 5);
+        row = r0 + warp + S * lane;
+        act = warp < S && row < ta.h;
+        rowc = act ? row : ta.h - 1;
+    };
+    // this thread's row of pixels (software-pipelined: the next tile's rows are requested before
+    // the current tile's flush)
+    uint32_t wd[NCH][4];
+    auto load_rows = [&](int fq, int txq, int rowq, uint32_t (&d)[NCH][4]) {
+        const uint8_t* src = ta.px + (long long)fq * ta.fstride + (long long)rowq * ta.pitch + txq * TCOLS;
+#pragma unroll
+        for (int c = 0; c < NCH; c += 2) ld256(src + 16 * c, &d[c][0]);
+    };
+    if (t0 < t1) {
+        int S, row, rowc;
+        bool act;
+        tile_rows(ty, S, row, act, rowc);
+        load_rows(f, tx, rowc, wd);
+    }
+
+    for (int nt = (int)(t1 - t0); nt > 0; --nt) {
+        if (f != cur_f) {  // CTA-uniform
+            if (kBox && cur_f >= 0) {
+                flush_box(bb, ta.boxes + 6 * cur_f);
+                bb = BoxAcc();
+            }
+            cur_f = f;
+            if (tid < 3) {
+                const FrameParams& fp = ta.fps[f];
+                const int k = tid;
+                const long long dc = fp.Dc[k];
+                s_fr.A[k] = fp.A[k];
+                s_fr.Dc[k] = dc;
+                s_fr.Dr[k] = fp.Dr[k];
+                const long long c1 = (long long)(TCOLS - 1) * dc;
+                s_fr.cmn[k] = min(0ll, c1);
+                s_fr.cmx[k] = max(0ll, c1);
+                s_fr.E[k] = (uint32_t)(dc < 0 ? -dc : dc);
+                s_fr.neg[k] = dc < 0 ? 0xffffffffu : 0u;
+                if (k == 0) {
+                    s_fr.te2 = fp.tie_eps + 1;
+                    s_fr.sx = dc < 0 ? 0u - 4u : 4u;
+                    s_fr.ok = fp.plane_ok && ((fp.lin_fit >> kShape) & 1);
+                    for (int q = 0; q < 4; ++q) s_fr.pz[q] = fp.pz[q];
+                }
+                if (k == 1) s_fr.sy = dc < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
+            }
+        }
+        __syncthreads();  // frame constants staged; table zeroed (first tile) or flushed
+        const int c0t = tx * TCOLS, r0t = ty * TROWS;
+        const int nr1 = min(TROWS, ta.h - r0t) - 1;  // last row of this tile, tile-relative
+        int lo[3], hi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const long long ut = s_fr.A[k] + (long long)r0t * s_fr.Dr[k] + (long long)c0t * s_fr.Dc[k];
+            const long long r1 = (long long)nr1 * s_fr.Dr[k];
+            // u is affine in (col, row): its fixed-point extremes over the tile sit at corners
+            lo[k] = (int)((ut + s_fr.cmn[k] + min(0ll, r1)) >> 32);
+            hi[k] = (int)((ut + s_fr.cmx[k] + max(0ll, r1)) >> 32);
+        }
+        const int X0 = lo[0], Y0 = lo[1], X = hi[0] - lo[0] + 1, Y = hi[1] - lo[1] + 1;
+        const bool tok = s_fr.ok && X <= kTabMaxX && Y <= kTabMaxY;
+        const bool tin = lo[0] >= 0 && hi[0] <= g.nx - 1 && lo[1] >= 0 && hi[1] <= g.ny - 1 &&
+                         lo[2] >= g.zb && hi[2] <= g.zb + g.nzl - 1;
+        int S, row, rowc;
+        bool act;
+        tile_rows(ty, S, row, act, rowc);
+        if (!act) {  // (idle warps and lanes past a short tile's end: add nothing)
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) wd[c][0] = wd[c][1] = wd[c][2] = wd[c][3] = 0u;
+        }
+        // fixed-point u at the start of chunk c of this thread's row
+        auto chunk_u = [&](int c, int k) -> long long {
+            return s_fr.A[k] + (long long)rowc * s_fr.Dr[k] + (long long)(c0t + 16 * c) * s_fr.Dc[k];
+        };
+        // per-chunk write mask: a chunk goes into the table when its whole index range lies inside
+        // the grid / slab; wholly outside -> counted out of bounds; straddling -> exact pass
+        uint32_t wmask = act && tok ? (1u << NCH) - 1u : 0u;
+        if (act && (!tok || !tin)) {
+            const int clo[3] = {0, 0, g.zb}, chi[3] = {g.nx - 1, g.ny - 1, g.zb + g.nzl - 1};
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                bool inb = true, out = false;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const long long u = chunk_u(c, k);
+                    const int i0 = (int)(u >> 32), i15 = (int)((u + 15ll * s_fr.Dc[k]) >> 32);
+                    // no margin needed: a tie-free chunk's fixed-point indices are the exact ones
+                    // and a tie chunk is undone and deferred after its walk; the exact index is
+                    // within 1 of the fixed-point one, so a range 2 outside misses the grid
+                    inb = inb && min(i0, i15) >= clo[k] && max(i0, i15) <= chi[k];
+                    out = out || max(i0, i15) + 1 < clo[k] || min(i0, i15) - 1 > chi[k];
+                }
+                if (!tok || !inb) {
+                    wmask &= ~(1u << c);
+                    if (out && tok) {
+                        atomicAdd(&s_cnt[0], 1u);
+                    } else {
+                        push_work(ta, f, row, (c0t >> 4) + c);
+                        atomicAdd(&s_cnt[1], 1u);
+                    }
+                    wd[c][0] = wd[c][1] = wd[c][2] = wd[c][3] = 0u;  // walked, adds nothing
+                }
+            }
+        }
+        if (tok && warp < S) {
+            const uint32_t e0 = s_fr.E[0], e1 = s_fr.E[1], e2 = s_fr.E[2], sx = s_fr.sx, sy = s_fr.sy;
+            const uint32_t tie2 = 2u * s_fr.te2;
+            // walk state at pixel 0 of the row
+            uint32_t w0, w1, w2, a;
+            walk_state(chunk_u(0, 0), chunk_u(0, 1), chunk_u(0, 2), s_fr, X0, Y0, w0, w1, w2, a);
+#if SVR_TILES_PREFETCH
+            if (tin) {  // L2 prefetch of the row's first voxel line: the flush's REDs then hit L2
+                const int ix = (int)(chunk_u(0, 0) >> 32), iy = (int)(chunk_u(0, 1) >> 32),
+                          iz = (int)(chunk_u(0, 2) >> 32);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ta.acc + (((long long)(iz - g.zb) * g.ny + iy) * g.nx + ix)));
+            }
+#endif
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                if (c > 0) tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
+                const uint32_t o20 = (wmask >> c) & 1u ? 0x00100000u : 0u;
+                uint32_t tmin = min(w0, min(w1, w2));
+                red_shared(tab + a, __byte_perm(wd[c][0], o20, 0x7640));
+#pragma unroll
+                for (int j = 1; j < kChunk; ++j) {
+                    tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
+                    tmin = min(tmin, min(w0, min(w1, w2)));
+                    red_shared(tab + a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                }
+                const bool tie = o20 != 0u && tmin < tie2;
+                if (__any_sync(0xffffffffu, tie)) {  // rare: undo the chunk, send it to the exact pass
+                    if (tie) {
+                        uint32_t v0, v1, v2, ua;  // state at the chunk's pixel 0 (= the walk's)
+                        walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, v0, v1, v2, ua);
+                        red_shared(tab + ua, 0u - __byte_perm(wd[c][0], o20, 0x7640));
+#pragma unroll
+                        for (int j = 1; j < kChunk; ++j) {  // (unrolled: wd stays in registers)
+                            tile_step(v0, v1, v2, ua, e0, e1, e2, sx, sy);
+                            red_shared(tab + ua, 0u - __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                        }
+                        push_work(ta, f, row, (c0t >> 4) + c);
+                        atomicAdd(&s_cnt[1], 1u);
+                    }
+                }
+                if (kBox && o20 != 0u && !tie) {
+                    {
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            const long long u = chunk_u(c, k);
+                            const int i0 = (int)(u >> 32), i15 = (int)((u + 15ll * s_fr.Dc[k]) >> 32);
+                            if (k == 0) { bb.x0 = min(bb.x0, min(i0, i15)); bb.x1 = max(bb.x1, max(i0, i15)); }
+                            if (k == 1) { bb.y0 = min(bb.y0, min(i0, i15)); bb.y1 = max(bb.y1, max(i0, i15)); }
+                            if (k == 2) { bb.z0 = min(bb.z0, min(i0, i15)); bb.z1 = max(bb.z1, max(i0, i15)); }
+                        }
+                    }
+                }
+            }
+        }
+        // next tile: advance and request its rows now (they arrive during this tile's flush)
+        const int fcur = f;
+        if (++tx == ta.ntx) {
+            tx = 0;
+            if (++ty == ta.nty) {
+                ty = 0;
+                ++f;
+            }
+        }
+        if (tid == 0) s_px += (unsigned long long)TCOLS * (unsigned long long)(nr1 + 1);
+        if (nt > 1) {
+            int Sn, rown, rowcn;
+            bool actn;
+            tile_rows(ty, Sn, rown, actn, rowcn);
+            load_rows(f, tx, rowcn, wd);
+        }
+        (void)fcur;
+        __syncthreads();  // table complete
+        if (tok) {
+            // flush + zero: positions p = x + X y spread over all threads, walked incrementally
+            const double zt = s_fr.pz[0] + s_fr.pz[1] * (double)X0 + s_fr.pz[2] * (double)Y0 - s_fr.pz[3];
+            const int zint = (int)floor(zt);
+            const float zf0 = (float)(zt - (double)zint);
+            const float p1 = (float)s_fr.pz[1], p2 = (float)s_fr.pz[2];
+            // a k = ceil(t) below kmin cannot occur: offsets from the base stay non-negative
+            const int kmin = -1 + (int)floorf(zf0 + fminf(0.f, p1 * (float)(X - 1)) + fminf(0.f, p2 * (float)(Y - 1)));
+            const long long sxy = (long long)g.nx * g.ny;
+            const uint32_t sxy8 = (uint32_t)(sxy * 8), nx8 = (uint32_t)g.nx * 8u;
+            const unsigned long long base =
+                (unsigned long long)ta.acc +
+                8ull * (unsigned long long)((long long)(zint + kmin - g.zb) * sxy + (long long)Y0 * g.nx + X0);
+            const int XY = X * Y;
+            const uint32_t zpar = (uint32_t)(zint + kmin) & 1u;
+            const float rX = 1.0f / (float)X;
+            // y = p / X exactly: the quotients' fractional parts are >= 1/(2X) from an integer
+            const int y0 = (int)(((float)tid + 0.5f) * rX);
+            int x = tid - y0 * X;
+            const int dy = (int)(((float)NT + 0.5f) * rX), dx = NT - dy * X;
+            int ti = x + kTabStr * y0;
+            uint32_t go = (uint32_t)y0 * nx8 + (uint32_t)x * 8u;
+            float tt = fmaf(p2, (float)y0, fmaf(p1, (float)x, zf0)) - (float)kmin;
+            const int dti = dx + kTabStr * dy, wti = kTabStr - X;
+            const uint32_t dgo = (uint32_t)dy * nx8 + (uint32_t)dx * 8u, wgo = nx8 - 8u * (uint32_t)X;
+            const float dtt = p1 * (float)dx + p2 * (float)dy, wtt = p2 - p1 * (float)X;
+            for (int p = tid; p < XY; p += NT) {
+                const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + kTabPlane];
+                s_tab[ti] = 0u;
+                s_tab[ti + kTabPlane] = 0u;
+                const uint32_t k = (uint32_t)(int)ceilf(tt);  // k - kmin >= 0
+                const bool odd = ((k ^ zpar) & 1u) != 0u;
+                const unsigned long long a0 = base + (k * sxy8 + go);
+                // per slot: an empty slot's voxel may lie outside the slab (face tiles), and a
+                // RED of 0 would still pull its line into L2 and write it back
+                const uint32_t vlo = odd ? v1 : v0, vhi = odd ? v0 : v1;
+                if (vlo) red_word(a0, vlo);
+                if (vhi) red_word(a0 + sxy8, vhi);
+                x += dx;
+                ti += dti;
+                go += dgo;
+                tt += dtt;
+                if (x >= X) {
+                    x -= X;
+                    ti += wti;
+                    go += wgo;
+                    tt += wtt;
+                }
+            }
+        }
+        __syncthreads();  // table clean, frame constants free for the next tile
+    }
+    if (kBox && cur_f >= 0) flush_box(bb, ta.boxes + 6 * cur_f);
+    if (tid == 0) {  // (after the loop's last barrier: s_cnt is final)
+        const ull oob = 16ull * s_cnt[0], def = s_cnt[1], n_px = s_px;
+        // every pixel of the CTA's tiles is inserted here unless counted out of bounds or deferred
+        // (k_pnn_work counts the deferred chunks' pixels)
+        if (n_px > oob + 16ull * def) atomicAdd(&ta.stats[kStInserted], n_px - oob - 16ull * def);
+        if (oob) atomicAdd(&ta.stats[kStOob], oob);
+        if (def) atomicAdd(&ta.stats[kStDeferred], def);
+    }
+}
+
+}  // namespace svr
