@@ -154,6 +154,8 @@ struct svr_volume {
     int plane_tw_cur = 4;       // the width chosen for the current insert call
     int lin_shapes_cur = 0;     // k_pnn_tiles shapes every frame of the current insert call fits
     int tiles_occ[8] = {};      // k_pnn_tiles resident CTAs per SM, per <shape, box> (lazy)
+    TileDesc* d_desc = nullptr; // k_pnn_tiles per-tile descriptors
+    long long desc_cap = 0;
     int plane_flush_lin = 1;    // SVR_PLANE_FLUSH: k_pnn_lin table flush, 1 linear over all threads, 0 lane = x
     int lin_small = 4;          // SVR_LIN_SMALL: launches of <= this many frames use 64-row k_pnn_lin tiles
     int plane_lin = 1;          // SVR_PLANE_LIN: k_pnn_lin for linear probes (1: 128-row tiles, 2: 64), 0 k_pnn_plane
@@ -726,6 +728,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFree(v->d_boxes);
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
+    cudaFree(v->d_desc);
     cudaFree(v->d_work);
     for (int i = 0; i < svr_volume::kTileSlots; ++i) {
         cudaFree(v->d_tiles[i]);
@@ -1083,6 +1086,18 @@ static void launch_rows_t(svr_volume* v, const uint8_t* px, long long pitch, lon
     v->launches++;
 }
 
+// per-tile descriptor buffer of k_pnn_tiles (grown outside any graph capture: fg_capture
+// pre-sizes it for one frame)
+static int ensure_desc(svr_volume* v, long long ntiles) {
+    if (v->desc_cap >= ntiles) return SVR_OK;
+    CK(cudaStreamSynchronize(v->stream));
+    cudaFree(v->d_desc);
+    v->d_desc = nullptr;
+    v->desc_cap = std::max<long long>(ntiles, 4096);
+    CK(cudaMalloc(&v->d_desc, sizeof(TileDesc) * v->desc_cap));
+    return SVR_OK;
+}
+
 // K1 for linear probes: k_pnn_tiles (persistent over the launch's tiles) + the exact pass.
 template <int NCH, int NW, bool kBox>
 static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
@@ -1093,8 +1108,9 @@ static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
         v->tiles_occ[slot] = std::max(1, occ);
     }
     const long long ctas = std::min<long long>(ta.ntiles, (long long)v->num_sms * v->tiles_occ[slot]);
+    k_tile_desc<NCH, NW><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->stream>>>(ta, const_cast<TileDesc*>(ta.desc));
     k_pnn_tiles<NCH, NW, kBox><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
-    v->launches++;
+    v->launches += 2;
     return SVR_OK;
 }
 
@@ -1125,6 +1141,8 @@ static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, l
     ta.work = v->d_work;
     ta.work_n = v->d_work_n;
     ta.work_cap = v->work_cap;
+    if (int e = ensure_desc(v, ta.ntiles)) return e;
+    ta.desc = v->d_desc;
     switch (shape + 4 * box) {
         case 0: return launch_tiles_t<4, 4, false>(v, ta);
         case 1: return launch_tiles_t<2, 4, false>(v, ta);
@@ -2123,6 +2141,7 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
         CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
     }
     if (int e = ensure_fan(v, c)) return e;
+    if (int e = ensure_desc(v, (long long)(w / 32 + 1) * (h / 64 + 1))) return e;
     // bounds with headroom: later frames of a sweep rarely need a larger graph
     f.fill_ctas = std::max(f.fill_ctas, nf + nf / 4 + 1);
     f.depth_ctas = std::max(f.depth_ctas, nd + nd / 4 + 1);

@@ -52,6 +52,20 @@ struct TilesArgs {
     ull* work;
     unsigned int* work_n;
     unsigned int work_cap;
+    const struct TileDesc* desc;  // per-tile constants (k_tile_desc)
+};
+
+// Per-tile constants, computed once per tile by k_tile_desc instead of redundantly by every warp
+// of the insert (the per-warp uniform setup had cost ~4 instructions per pixel).
+struct __align__(16) TileDesc {
+    long long Ut[3];        // 32.32 fixed u at the tile's (col, row) origin, +1/2
+    long long base;         // flush base: byte offset of voxel (X0, Y0, zint + kmin) in the slab
+    int X0, Y0;             // table origin (voxel), the tile's fixed-point index minima
+    int XY;                 // X | Y << 16: table extent
+    int flags;              // bit 0 tok (table usable), bit 1 tin (inside grid / slab)
+    int zpar;               // (zint + kmin) & 1
+    float tt0;              // z_c - h at the table origin, minus kmin (flush plane offset)
+    int pad[2];
 };
 
 // one exact step of the three fractions; the table byte address follows the carries
@@ -71,18 +85,66 @@ __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& 
 // A frame's constants, staged in shared memory when a CTA's tile range enters the frame (keeps
 // the 64-register budget for the walk).
 struct TileFrame {
-    long long A[3], Dc[3], Dr[3];  // 32.32 fixed: u(0,0) + 1/2, du/dcol, du/drow
-    long long cmn[3], cmx[3];      // min / max of (TCOLS - 1) Dc over {0, 1}
-    double pz[4];                  // frame plane (FrameParams::pz)
+    long long Dc[3], Dr[3];        // 32.32 fixed: du/dcol, du/drow
     uint32_t E[3], neg[3];         // |Dc| low words; all-ones when Dc < 0 (mirrored fractions)
     uint32_t te2, sx, sy;          // tie window + 1; table byte steps along x and y
-    int ok;                        // plane_ok and this tile shape fits (FrameParams::lin_fit)
+    float p1, p2;                  // frame plane slopes (FrameParams::pz[1], pz[2])
 };
 
 __device__ __forceinline__ void push_work(const TilesArgs& ta, int f, int row, int cc) {
     // the host sizes the list for every chunk of the launch, so it cannot overflow
     const unsigned int slot = atomicAdd(ta.work_n, 1u);
     ta.work[slot] = work_entry(f, row, cc, 0xffffu);
+}
+
+template <int NCH, int NW>
+__global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc* __restrict__ out) {
+    constexpr int TROWS = 32 * NW, TCOLS = 16 * NCH;
+    constexpr int kShape = (NCH == 2) + 2 * (NW == 2);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ta.ntiles) return;
+    const int tpf = ta.ntx * ta.nty;
+    const int f = (int)(t / tpf), rem = (int)(t - (long long)f * tpf);
+    const int ty = rem / ta.ntx, tx = rem - ty * ta.ntx;
+    const FrameParams& fp = ta.fps[f];
+    const GridDev& g = ta.g;
+    const int c0t = tx * TCOLS, r0t = ty * TROWS;
+    const int nr1 = min(TROWS, ta.h - r0t) - 1;
+    TileDesc d;
+    int lo[3], hi[3];
+    bool ok = fp.plane_ok && ((fp.lin_fit >> kShape) & 1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const long long dc = fp.Dc[k], dr = fp.Dr[k];
+        d.Ut[k] = fp.A[k] + (long long)r0t * dr + (long long)c0t * dc;
+        const long long c1 = (long long)(TCOLS - 1) * dc, r1 = (long long)nr1 * dr;
+        // u is affine in (col, row): its fixed-point extremes over the tile sit at corners
+        lo[k] = (int)((d.Ut[k] + min(0ll, c1) + min(0ll, r1)) >> 32);
+        hi[k] = (int)((d.Ut[k] + max(0ll, c1) + max(0ll, r1)) >> 32);
+        ok = ok && (unsigned long long)(dc < 0 ? -dc : dc) < (1ull << 32);
+    }
+    const int X = hi[0] - lo[0] + 1, Y = hi[1] - lo[1] + 1;
+    ok = ok && X <= kTabMaxX && Y <= kTabMaxY;
+    const bool tin = lo[0] >= 0 && hi[0] <= g.nx - 1 && lo[1] >= 0 && hi[1] <= g.ny - 1 &&
+                     lo[2] >= g.zb && hi[2] <= g.zb + g.nzl - 1;
+    d.X0 = lo[0];
+    d.Y0 = lo[1];
+    d.XY = X | (Y << 16);
+    d.flags = (ok ? 1 : 0) | (tin ? 2 : 0);
+    // flush plane: the column (x, y) holds voxels z in [z_c - h, z_c + h] (2h < 2), z_c - h =
+    // zint + tt0 + kmin + p1 x + p2 y (x, y table-relative; fp32 relative to the tile corner, error
+    // ~2e-5 against the 2e-3 margin in pz3); k = ceil(tt) >= 0 for every table position
+    const double zt = fp.pz[0] + fp.pz[1] * (double)lo[0] + fp.pz[2] * (double)lo[1] - fp.pz[3];
+    const int zint = (int)floor(zt);
+    const float zf0 = (float)(zt - (double)zint);
+    const float p1 = (float)fp.pz[1], p2 = (float)fp.pz[2];
+    const int kmin = -1 + (int)floorf(zf0 + fminf(0.f, p1 * (float)(X - 1)) + fminf(0.f, p2 * (float)(Y - 1)));
+    d.tt0 = zf0 - (float)kmin;
+    d.zpar = (zint + kmin) & 1;
+    const long long sxy = (long long)g.nx * g.ny;
+    d.base = 8ll * ((long long)(zint + kmin - g.zb) * sxy + (long long)lo[1] * g.nx + lo[0]);
+    d.pad[0] = d.pad[1] = 0;
+    out[t] = d;
 }
 
 // Walk state (fractions + table byte address) of the pixel whose fixed-point u is (u0, u1, u2).
@@ -123,11 +185,11 @@ __device__ __forceinline__ void red_word(unsigned long long addr, uint32_t v) {
 template <int NCH, int NW, bool kBox>
 __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB) k_pnn_tiles(const TilesArgs ta) {
     constexpr int NT = 32 * NW, TROWS = 32 * NW, TCOLS = 16 * NCH;
-    constexpr int kShape = (NCH == 2) + 2 * (NW == 2);
     __shared__ __align__(16) uint32_t s_tab[2 * kTabPlane];
     __shared__ TileFrame s_fr;
-    __shared__ unsigned int s_cnt[2];  // chunks counted out of bounds / deferred (rare: no registers)
+    __shared__ unsigned int s_cnt[2];    // chunks counted out of bounds / deferred (rare)
     __shared__ unsigned long long s_px;  // pixels of this CTA's tiles
+    __shared__ TileDesc s_desc[2];       // current / next tile's descriptor (cp.async-staged)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 2) s_cnt[tid] = 0u;
     if (tid == 0) s_px = 0ull;
@@ -153,22 +215,35 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         act = warp < S && row < ta.h;
         rowc = act ? row : ta.h - 1;
     };
-    // this thread's row of pixels (software-pipelined: the next tile's rows are requested before
-    // the current tile's flush)
+    // this thread's row of pixels (software-pipelined: the next tile's rows and descriptor are
+    // requested before the current tile's flush)
     uint32_t wd[NCH][4];
     auto load_rows = [&](int fq, int txq, int rowq, uint32_t (&d)[NCH][4]) {
         const uint8_t* src = ta.px + (long long)fq * ta.fstride + (long long)rowq * ta.pitch + txq * TCOLS;
 #pragma unroll
         for (int c = 0; c < NCH; c += 2) ld256(src + 16 * c, &d[c][0]);
     };
+    // threads 0..3 stage a tile descriptor (4 x 16 B) into shared memory with cp.async
+    auto stage_desc = [&](long long t, int b) {
+        if (tid < 4) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4*>(&s_desc[b]) + tid);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(reinterpret_cast<const uint4*>(ta.desc + t) + tid) : "memory");
+        }
+    };
+    auto wait_desc = [&]() {
+        if (tid < 4) asm volatile("cp.async.wait_all;" ::: "memory");
+    };
     if (t0 < t1) {
         int S, row, rowc;
         bool act;
         tile_rows(ty, S, row, act, rowc);
         load_rows(f, tx, rowc, wd);
+        stage_desc(t0, 0);
+        wait_desc();
     }
 
-    for (int nt = (int)(t1 - t0); nt > 0; --nt) {
+    for (long long t = t0; t < t1; ++t) {
         if (f != cur_f) {  // CTA-uniform
             if (kBox && cur_f >= 0) {
                 flush_box(bb, ta.boxes + 6 * cur_f);
@@ -179,39 +254,25 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 const FrameParams& fp = ta.fps[f];
                 const int k = tid;
                 const long long dc = fp.Dc[k];
-                s_fr.A[k] = fp.A[k];
                 s_fr.Dc[k] = dc;
                 s_fr.Dr[k] = fp.Dr[k];
-                const long long c1 = (long long)(TCOLS - 1) * dc;
-                s_fr.cmn[k] = min(0ll, c1);
-                s_fr.cmx[k] = max(0ll, c1);
                 s_fr.E[k] = (uint32_t)(dc < 0 ? -dc : dc);
                 s_fr.neg[k] = dc < 0 ? 0xffffffffu : 0u;
                 if (k == 0) {
                     s_fr.te2 = fp.tie_eps + 1;
                     s_fr.sx = dc < 0 ? 0u - 4u : 4u;
-                    s_fr.ok = fp.plane_ok && ((fp.lin_fit >> kShape) & 1);
-                    for (int q = 0; q < 4; ++q) s_fr.pz[q] = fp.pz[q];
+                    s_fr.p1 = (float)fp.pz[1];
+                    s_fr.p2 = (float)fp.pz[2];
                 }
                 if (k == 1) s_fr.sy = dc < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
             }
         }
-        __syncthreads();  // frame constants staged; table zeroed (first tile) or flushed
+        __syncthreads();  // frame constants + descriptor staged; table zeroed or flushed
+        const TileDesc& dsc = s_desc[(int)(t - t0) & 1];
+        if (t + 1 < t1) stage_desc(t + 1, (int)(t + 1 - t0) & 1);
         const int c0t = tx * TCOLS, r0t = ty * TROWS;
-        const int nr1 = min(TROWS, ta.h - r0t) - 1;  // last row of this tile, tile-relative
-        int lo[3], hi[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const long long ut = s_fr.A[k] + (long long)r0t * s_fr.Dr[k] + (long long)c0t * s_fr.Dc[k];
-            const long long r1 = (long long)nr1 * s_fr.Dr[k];
-            // u is affine in (col, row): its fixed-point extremes over the tile sit at corners
-            lo[k] = (int)((ut + s_fr.cmn[k] + min(0ll, r1)) >> 32);
-            hi[k] = (int)((ut + s_fr.cmx[k] + max(0ll, r1)) >> 32);
-        }
-        const int X0 = lo[0], Y0 = lo[1], X = hi[0] - lo[0] + 1, Y = hi[1] - lo[1] + 1;
-        const bool tok = s_fr.ok && X <= kTabMaxX && Y <= kTabMaxY;
-        const bool tin = lo[0] >= 0 && hi[0] <= g.nx - 1 && lo[1] >= 0 && hi[1] <= g.ny - 1 &&
-                         lo[2] >= g.zb && hi[2] <= g.zb + g.nzl - 1;
+        const int X0 = dsc.X0, Y0 = dsc.Y0, X = dsc.XY & 0xffff, Y = dsc.XY >> 16;
+        const bool tok = dsc.flags & 1, tin = dsc.flags & 2;
         int S, row, rowc;
         bool act;
         tile_rows(ty, S, row, act, rowc);
@@ -220,8 +281,9 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             for (int c = 0; c < NCH; ++c) wd[c][0] = wd[c][1] = wd[c][2] = wd[c][3] = 0u;
         }
         // fixed-point u at the start of chunk c of this thread's row
+        const int rrel = rowc - r0t;
         auto chunk_u = [&](int c, int k) -> long long {
-            return s_fr.A[k] + (long long)rowc * s_fr.Dr[k] + (long long)(c0t + 16 * c) * s_fr.Dc[k];
+            return dsc.Ut[k] + (long long)rrel * s_fr.Dr[k] + (long long)(16 * c) * s_fr.Dc[k];
         };
         // per-chunk write mask: a chunk goes into the table when its whole index range lies inside
         // the grid / slab; wholly outside -> counted out of bounds; straddling -> exact pass
@@ -258,14 +320,16 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             const uint32_t tie2 = 2u * s_fr.te2;
             // walk state at pixel 0 of the row
             uint32_t w0, w1, w2, a;
-            walk_state(chunk_u(0, 0), chunk_u(0, 1), chunk_u(0, 2), s_fr, X0, Y0, w0, w1, w2, a);
+            {
+                const long long u0 = chunk_u(0, 0), u1 = chunk_u(0, 1), u2 = chunk_u(0, 2);
+                walk_state(u0, u1, u2, s_fr, X0, Y0, w0, w1, w2, a);
 #if SVR_TILES_PREFETCH
-            if (tin) {  // L2 prefetch of the row's first voxel line: the flush's REDs then hit L2
-                const int ix = (int)(chunk_u(0, 0) >> 32), iy = (int)(chunk_u(0, 1) >> 32),
-                          iz = (int)(chunk_u(0, 2) >> 32);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ta.acc + (((long long)(iz - g.zb) * g.ny + iy) * g.nx + ix)));
-            }
+                if (tin) {  // L2 prefetch of the row's first voxel line: the flush's REDs then hit L2
+                    const int ix = (int)(u0 >> 32), iy = (int)(u1 >> 32), iz = (int)(u2 >> 32);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(ta.acc + (((long long)(iz - g.zb) * g.ny + iy) * g.nx + ix)));
+                }
 #endif
+            }
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 if (c > 0) tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
@@ -294,21 +358,22 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                     }
                 }
                 if (kBox && o20 != 0u && !tie) {
-                    {
 #pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            const long long u = chunk_u(c, k);
-                            const int i0 = (int)(u >> 32), i15 = (int)((u + 15ll * s_fr.Dc[k]) >> 32);
-                            if (k == 0) { bb.x0 = min(bb.x0, min(i0, i15)); bb.x1 = max(bb.x1, max(i0, i15)); }
-                            if (k == 1) { bb.y0 = min(bb.y0, min(i0, i15)); bb.y1 = max(bb.y1, max(i0, i15)); }
-                            if (k == 2) { bb.z0 = min(bb.z0, min(i0, i15)); bb.z1 = max(bb.z1, max(i0, i15)); }
-                        }
+                    for (int k = 0; k < 3; ++k) {
+                        const long long u = chunk_u(c, k);
+                        const int i0 = (int)(u >> 32), i15 = (int)((u + 15ll * s_fr.Dc[k]) >> 32);
+                        if (k == 0) { bb.x0 = min(bb.x0, min(i0, i15)); bb.x1 = max(bb.x1, max(i0, i15)); }
+                        if (k == 1) { bb.y0 = min(bb.y0, min(i0, i15)); bb.y1 = max(bb.y1, max(i0, i15)); }
+                        if (k == 2) { bb.z0 = min(bb.z0, min(i0, i15)); bb.z1 = max(bb.z1, max(i0, i15)); }
                     }
                 }
             }
         }
-        // next tile: advance and request its rows now (they arrive during this tile's flush)
-        const int fcur = f;
+        if (tid == 0) s_px += (unsigned long long)TCOLS * (unsigned long long)(min(TROWS, ta.h - r0t));
+        // flush constants of this tile, then the next tile's rows + descriptor are requested
+        const unsigned long long fbase = (unsigned long long)ta.acc + (unsigned long long)dsc.base;
+        const uint32_t zpar = (uint32_t)dsc.zpar;
+        const float tt0 = dsc.tt0;
         if (++tx == ta.ntx) {
             tx = 0;
             if (++ty == ta.nty) {
@@ -316,30 +381,19 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 ++f;
             }
         }
-        if (tid == 0) s_px += (unsigned long long)TCOLS * (unsigned long long)(nr1 + 1);
-        if (nt > 1) {
+        if (t + 1 < t1) {
             int Sn, rown, rowcn;
             bool actn;
             tile_rows(ty, Sn, rown, actn, rowcn);
             load_rows(f, tx, rowcn, wd);
+            wait_desc();
         }
-        (void)fcur;
         __syncthreads();  // table complete
         if (tok) {
             // flush + zero: positions p = x + X y spread over all threads, walked incrementally
-            const double zt = s_fr.pz[0] + s_fr.pz[1] * (double)X0 + s_fr.pz[2] * (double)Y0 - s_fr.pz[3];
-            const int zint = (int)floor(zt);
-            const float zf0 = (float)(zt - (double)zint);
-            const float p1 = (float)s_fr.pz[1], p2 = (float)s_fr.pz[2];
-            // a k = ceil(t) below kmin cannot occur: offsets from the base stay non-negative
-            const int kmin = -1 + (int)floorf(zf0 + fminf(0.f, p1 * (float)(X - 1)) + fminf(0.f, p2 * (float)(Y - 1)));
-            const long long sxy = (long long)g.nx * g.ny;
-            const uint32_t sxy8 = (uint32_t)(sxy * 8), nx8 = (uint32_t)g.nx * 8u;
-            const unsigned long long base =
-                (unsigned long long)ta.acc +
-                8ull * (unsigned long long)((long long)(zint + kmin - g.zb) * sxy + (long long)Y0 * g.nx + X0);
+            const float p1 = s_fr.p1, p2 = s_fr.p2;
+            const uint32_t sxy8 = (uint32_t)((long long)g.nx * g.ny * 8), nx8 = (uint32_t)g.nx * 8u;
             const int XY = X * Y;
-            const uint32_t zpar = (uint32_t)(zint + kmin) & 1u;
             const float rX = 1.0f / (float)X;
             // y = p / X exactly: the quotients' fractional parts are >= 1/(2X) from an integer
             const int y0 = (int)(((float)tid + 0.5f) * rX);
@@ -347,7 +401,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             const int dy = (int)(((float)NT + 0.5f) * rX), dx = NT - dy * X;
             int ti = x + kTabStr * y0;
             uint32_t go = (uint32_t)y0 * nx8 + (uint32_t)x * 8u;
-            float tt = fmaf(p2, (float)y0, fmaf(p1, (float)x, zf0)) - (float)kmin;
+            float tt = fmaf(p2, (float)y0, fmaf(p1, (float)x, tt0));
             const int dti = dx + kTabStr * dy, wti = kTabStr - X;
             const uint32_t dgo = (uint32_t)dy * nx8 + (uint32_t)dx * 8u, wgo = nx8 - 8u * (uint32_t)X;
             const float dtt = p1 * (float)dx + p2 * (float)dy, wtt = p2 - p1 * (float)X;
@@ -357,7 +411,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 s_tab[ti + kTabPlane] = 0u;
                 const uint32_t k = (uint32_t)(int)ceilf(tt);  // k - kmin >= 0
                 const bool odd = ((k ^ zpar) & 1u) != 0u;
-                const unsigned long long a0 = base + (k * sxy8 + go);
+                const unsigned long long a0 = fbase + (k * sxy8 + go);
                 // per slot: an empty slot's voxel may lie outside the slab (face tiles), and a
                 // RED of 0 would still pull its line into L2 and write it back
                 const uint32_t vlo = odd ? v1 : v0, vhi = odd ? v0 : v1;
