@@ -33,10 +33,16 @@
 
 namespace svr {
 
-constexpr int kTabStr = 33;                    // table row stride in words (odd)
-constexpr int kTabPlane = 2048;                // words per parity plane: byte offset bit 13
-constexpr int kTabMaxY = kTabPlane / kTabStr;  // 62 voxel rows
+// Table layout: word (x + kTabStr y) of parity plane p (planes 16 KB apart) holds voxel column
+// (x, y)'s slot of z parity p.  The walk's byte address is absolute (no base add per pixel) and a
+// z step XORs its bit 14: plane 0 spans [tab, tab + 8 KB) with tab < 8 KB (static shared memory
+// starts at the CTA's 1 KB reserved area; checked per CTA), so bit 14 is 0 there and 1 in plane 1.
+// kTabStr is odd, so rows 1-2 voxels apart (a warp's lanes) fall into distinct banks.
+constexpr int kTabStr = 33;                    // table row stride in words
+constexpr int kTabPlane = 4096;                // words between the parity planes (bit 14)
+constexpr int kTabMaxY = 62;                   // voxel rows (62 * 33 <= 2048 words per plane)
 constexpr int kTabMaxX = 32;                   // voxel columns
+constexpr int kTabWords = kTabPlane + 2048;    // 24 KB (the 8 KB gap is unused)
 
 struct TilesArgs {
     const uint8_t* px;
@@ -77,7 +83,7 @@ __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& 
         "add.cc.u32 %1, %1, %5;\n\taddc.u32 c1, 0, 0;\n\t"
         "add.cc.u32 %2, %2, %6;\n\taddc.u32 c2, 0, 0;\n\t"
         "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
-        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 xor.b32 %3, %3, 8192;\n\t}"
+        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 xor.b32 %3, %3, 16384;\n\t}"
         : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a)
         : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy));
 }
@@ -152,8 +158,8 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
 // upper half of the tie window) the index is already one step further, so later pixels' indices
 // stay exact no matter where the row starts (the pixel itself is a tie and gets deferred).
 __device__ __forceinline__ void walk_state(long long u0, long long u1, long long u2, const TileFrame& fr,
-                                           int X0, int Y0, uint32_t& w0, uint32_t& w1, uint32_t& w2,
-                                           uint32_t& a) {
+                                           int X0, int Y0, uint32_t tab, uint32_t& w0, uint32_t& w1,
+                                           uint32_t& w2, uint32_t& a) {
     const uint32_t te2 = fr.te2;
     const uint32_t m0 = (uint32_t)u0 ^ fr.neg[0], m1 = (uint32_t)u1 ^ fr.neg[1], m2 = (uint32_t)u2 ^ fr.neg[2];
     w0 = m0 + te2;
@@ -163,7 +169,7 @@ __device__ __forceinline__ void walk_state(long long u0, long long u1, long long
     const int ix = (int)(u0 >> 32) + (w0 < te2 ? (fr.neg[0] ? -1 : 1) : 0);
     const int iy = (int)(u1 >> 32) + (w1 < te2 ? (fr.neg[1] ? -1 : 1) : 0);
     const int iz = (int)(u2 >> 32) + (w2 < te2 ? 1 : 0);  // (only the parity matters)
-    a = 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + ((uint32_t)(iz & 1) << 13);
+    a = tab + 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + ((uint32_t)(iz & 1) << 14);
 }
 
 // 32-byte row segment load (one LDG.256, L1 no-allocate: every byte is read once)
@@ -185,7 +191,7 @@ __device__ __forceinline__ void red_word(unsigned long long addr, uint32_t v) {
 template <int NCH, int NW, bool kBox>
 __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB) k_pnn_tiles(const TilesArgs ta) {
     constexpr int NT = 32 * NW, TROWS = 32 * NW, TCOLS = 16 * NCH;
-    __shared__ __align__(16) uint32_t s_tab[2 * kTabPlane];
+    __shared__ __align__(16) uint32_t s_tab[kTabWords];
     __shared__ TileFrame s_fr;
     __shared__ unsigned int s_cnt[2];    // chunks counted out of bounds / deferred (rare)
     __shared__ unsigned long long s_px;  // pixels of this CTA's tiles
@@ -193,9 +199,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 2) s_cnt[tid] = 0u;
     if (tid == 0) s_px = 0ull;
-    for (int i = tid; i < 2 * kTabPlane / 4; i += NT)
+    for (int i = tid; i < kTabWords / 4; i += NT)
         reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0u, 0u, 0u, 0u);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(s_tab);
+    // (the XOR parity needs plane 0 below 16 KB - 8 KB; otherwise every tile takes the exact pass)
+    const bool tab_ok = tab + 4u * 2048u <= 16384u;
     const GridDev& g = ta.g;
     const int tpf = ta.ntx * ta.nty;
     const long long t0 = (long long)blockIdx.x * ta.ntiles / gridDim.x;
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         if (t + 1 < t1) stage_desc(t + 1, (int)(t + 1 - t0) & 1);
         const int c0t = tx * TCOLS, r0t = ty * TROWS;
         const int X0 = dsc.X0, Y0 = dsc.Y0, X = dsc.XY & 0xffff, Y = dsc.XY >> 16;
-        const bool tok = dsc.flags & 1, tin = dsc.flags & 2;
+        const bool tok = (dsc.flags & 1) && tab_ok, tin = dsc.flags & 2;
         int S, row, rowc;
         bool act;
         tile_rows(ty, S, row, act, rowc);
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             uint32_t w0, w1, w2, a;
             {
                 const long long u0 = chunk_u(0, 0), u1 = chunk_u(0, 1), u2 = chunk_u(0, 2);
-                walk_state(u0, u1, u2, s_fr, X0, Y0, w0, w1, w2, a);
+                walk_state(u0, u1, u2, s_fr, X0, Y0, tab, w0, w1, w2, a);
 #if SVR_TILES_PREFETCH
                 if (tin) {  // L2 prefetch of the row's first voxel line: the flush's REDs then hit L2
                     const int ix = (int)(u0 >> 32), iy = (int)(u1 >> 32), iz = (int)(u2 >> 32);
@@ -335,23 +343,23 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 if (c > 0) tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
                 const uint32_t o20 = (wmask >> c) & 1u ? 0x00100000u : 0u;
                 uint32_t tmin = min(w0, min(w1, w2));
-                red_shared(tab + a, __byte_perm(wd[c][0], o20, 0x7640));
+                red_shared(a, __byte_perm(wd[c][0], o20, 0x7640));
 #pragma unroll
                 for (int j = 1; j < kChunk; ++j) {
                     tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
                     tmin = min(tmin, min(w0, min(w1, w2)));
-                    red_shared(tab + a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                    red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
                 }
                 const bool tie = o20 != 0u && tmin < tie2;
                 if (__any_sync(0xffffffffu, tie)) {  // rare: undo the chunk, send it to the exact pass
                     if (tie) {
                         uint32_t v0, v1, v2, ua;  // state at the chunk's pixel 0 (= the walk's)
-                        walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, v0, v1, v2, ua);
-                        red_shared(tab + ua, 0u - __byte_perm(wd[c][0], o20, 0x7640));
+                        walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, v0, v1, v2, ua);
+                        red_shared(ua, 0u - __byte_perm(wd[c][0], o20, 0x7640));
 #pragma unroll
                         for (int j = 1; j < kChunk; ++j) {  // (unrolled: wd stays in registers)
                             tile_step(v0, v1, v2, ua, e0, e1, e2, sx, sy);
-                            red_shared(tab + ua, 0u - __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                            red_shared(ua, 0u - __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
                         }
                         push_work(ta, f, row, (c0t >> 4) + c);
                         atomicAdd(&s_cnt[1], 1u);
