@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SVR_ABI_VERSION 1
+#define SVR_ABI_VERSION 2
 
 /* return codes (core.hpp:12-32 exit-code mapping) */
 #define SVR_OK 0
@@ -99,6 +99,7 @@ typedef struct svr_stats {
     uint64_t exact_fallbacks;  /* pixels resolved by the exact fp64 chain (near .5 ties) */
     uint64_t kernel_launches;  /* kernels this handle launched (all kinds) */
     uint64_t chunks_deferred;  /* 16-px chunks sent to the exact per-pixel pass (ties, edges) */
+    uint64_t tiles_table;      /* B-scan tiles inserted through the shared-table kernel (K1) */
 } svr_stats;
 
 /* Depth-band coronal render (BASELINE cfg4).  Depth axis = grid y, depth(y) = y*voxel_mm.

@@ -52,6 +52,8 @@ def lib():
         L.orc_insert_frame.argtypes = [PG, P, C.c_int64, C.c_int32, C.c_int32, PR, PC, C.c_int32, PB]
         L.orc_insert_frames_mt.argtypes = [PG, P, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                            C.c_int32, PR, PC, C.c_int32, C.c_int32]
+        L.orc_insert_frames_mt_boxes.argtypes = [PG, P, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                                 C.c_int32, PR, PC, C.c_int32, C.c_int32, PB]
         L.orc_fill_holes.argtypes = [PG, PB, C.c_int32, C.c_int32]
         L.orc_fill_holes.restype = C.c_int64
         L.orc_values.argtypes = [PG, C.c_int32, P]
@@ -156,6 +158,20 @@ class OracleGrid:
                                         rigid_ptr(pa), C.byref(calib), int(skip_zero), nthreads)
         if rc:
             raise ValueError("oracle insert rejected input")
+
+    def insert_frames_mt_boxes(self, frames, poses, calib, skip_zero=False, nthreads=None):
+        """Multithreaded insert that also returns each frame's tight dirty box."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        n, h, w = frames.shape
+        pa = rigid_array(poses)
+        nthreads = nthreads or os.cpu_count() or 1
+        boxes = (Box * max(n, 1))()
+        rc = lib().orc_insert_frames_mt_boxes(C.byref(self.g), frames.ctypes.data, w, w * h, w, h, n,
+                                              rigid_ptr(pa), C.byref(calib), int(skip_zero), nthreads,
+                                              boxes)
+        if rc:
+            raise ValueError("oracle insert rejected input")
+        return [boxes[k] for k in range(n)]
 
     def insert_trilinear(self, frame, pose, calib, skip_zero=False):
         frame = np.ascontiguousarray(frame, dtype=np.uint8)

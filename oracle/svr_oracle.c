@@ -178,6 +178,7 @@ typedef struct {
     const svr_calib* c;
     const double *fs, *fc;
     uint64_t inserted, skipped;
+    svr_box* boxes; /* per-frame partial dirty boxes of this thread's planes (or NULL) */
 } mt_job;
 
 /* z-range (global planes, conservative) a frame can touch: the affine image of the pixel
@@ -234,6 +235,21 @@ static void* mt_worker(void* arg) {
                 g->sum[lin] += v;
                 g->count[lin] += 1;
                 j->inserted++;
+                if (j->boxes) {
+                    svr_box* b = &j->boxes[k];
+                    if (b->x0 > b->x1) {
+                        b->x0 = b->x1 = idx[0];
+                        b->y0 = b->y1 = idx[1];
+                        b->z0 = b->z1 = idx[2];
+                    } else {
+                        if (idx[0] < b->x0) b->x0 = idx[0];
+                        if (idx[0] > b->x1) b->x1 = idx[0];
+                        if (idx[1] < b->y0) b->y0 = idx[1];
+                        if (idx[1] > b->y1) b->y1 = idx[1];
+                        if (idx[2] < b->z0) b->z0 = idx[2];
+                        if (idx[2] > b->z1) b->z1 = idx[2];
+                    }
+                }
             }
         }
     }
@@ -243,6 +259,16 @@ static void* mt_worker(void* arg) {
 int orc_insert_frames_mt(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t stride,
                          int32_t w, int32_t h, int32_t nframes, const svr_rigid* poses,
                          const svr_calib* c, int32_t skip_zero, int32_t nthreads) {
+    return orc_insert_frames_mt_boxes(g, px, pitch, stride, w, h, nframes, poses, c, skip_zero,
+                                      nthreads, NULL);
+}
+
+/* orc_insert_frames_mt with the tight per-frame dirty boxes (insert_frame's DirtyRegion,
+ * SPEC.md:292) merged from the threads' partial boxes; boxes may be NULL. */
+int orc_insert_frames_mt_boxes(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t stride,
+                               int32_t w, int32_t h, int32_t nframes, const svr_rigid* poses,
+                               const svr_calib* c, int32_t skip_zero, int32_t nthreads,
+                               svr_box* boxes) {
     if (w != c->crop_w || h != c->crop_h) return SVR_E_INVALID;
     if (nthreads < 1) nthreads = 1;
     double* fs = NULL;
@@ -256,7 +282,14 @@ int orc_insert_frames_mt(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t 
     pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
     for (int t = 0; t < nthreads; ++t) {
         mt_job jb = {g, px, pitch, stride, w, h, nframes, skip_zero, t, nthreads, poses, c,
-                     fs, fc, 0, 0};
+                     fs, fc, 0, 0, NULL};
+        if (boxes) {
+            jb.boxes = (svr_box*)malloc(sizeof(svr_box) * (size_t)(nframes > 0 ? nframes : 1));
+            for (int32_t k = 0; k < nframes; ++k) {
+                svr_box e = {1, 1, 1, 0, 0, 0};
+                jb.boxes[k] = e;
+            }
+        }
         jobs[t] = jb;
         pthread_create(&th[t], NULL, mt_worker, &jobs[t]);
     }
@@ -277,6 +310,27 @@ int orc_insert_frames_mt(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t 
         uint64_t ins = 0;
         for (int t = 0; t < nthreads; ++t) ins += jobs[t].inserted;
         g->oob += nz - ins;
+    }
+    if (boxes) {
+        for (int32_t k = 0; k < nframes; ++k) {
+            svr_box m = {1, 1, 1, 0, 0, 0};
+            for (int t = 0; t < nthreads; ++t) {
+                const svr_box b = jobs[t].boxes[k];
+                if (b.x0 > b.x1) continue;
+                if (m.x0 > m.x1) {
+                    m = b;
+                } else {
+                    if (b.x0 < m.x0) m.x0 = b.x0;
+                    if (b.y0 < m.y0) m.y0 = b.y0;
+                    if (b.z0 < m.z0) m.z0 = b.z0;
+                    if (b.x1 > m.x1) m.x1 = b.x1;
+                    if (b.y1 > m.y1) m.y1 = b.y1;
+                    if (b.z1 > m.z1) m.z1 = b.z1;
+                }
+            }
+            boxes[k] = m;
+        }
+        for (int t = 0; t < nthreads; ++t) free(jobs[t].boxes);
     }
     g->frames += (uint64_t)nframes;
     free(jobs);

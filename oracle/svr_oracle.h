@@ -56,6 +56,10 @@ int orc_insert_frame(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, i
 int orc_insert_frames_mt(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t frame_stride,
                          int32_t w, int32_t h, int32_t nframes, const svr_rigid* poses,
                          const svr_calib* calib, int32_t skip_zero, int32_t nthreads);
+int orc_insert_frames_mt_boxes(orc_grid* g, const uint8_t* px, int64_t pitch, int64_t frame_stride,
+                               int32_t w, int32_t h, int32_t nframes, const svr_rigid* poses,
+                               const svr_calib* calib, int32_t skip_zero, int32_t nthreads,
+                               svr_box* boxes);
 int64_t orc_fill_holes(orc_grid* g, const svr_box* region, int32_t mode, int32_t radius);
 void orc_values(const orc_grid* g, int32_t apply_fills, uint8_t* out);
 

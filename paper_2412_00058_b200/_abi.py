@@ -65,7 +65,8 @@ class Stats(C.Structure):
     _fields_ = [("frames_inserted", C.c_uint64), ("pixels_inserted", C.c_uint64),
                 ("pixels_oob", C.c_uint64), ("pixels_skipped_zero", C.c_uint64),
                 ("pixels_saturated", C.c_uint64), ("exact_fallbacks", C.c_uint64),
-                ("kernel_launches", C.c_uint64), ("chunks_deferred", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("chunks_deferred", C.c_uint64),
+                ("tiles_table", C.c_uint64)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
@@ -164,7 +165,7 @@ def lib() -> C.CDLL:
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
-            if L.svr_abi_version() != 1:
+            if L.svr_abi_version() != 2:
                 raise RuntimeError("libspinevol_b200 ABI version mismatch")
             _lib = L
     return _lib

@@ -2050,6 +2050,7 @@ extern "C" int svr_get_stats(svr_volume* v, svr_stats* out) {
     out->exact_fallbacks = h[kStFallback];
     out->kernel_launches = v->launches;
     out->chunks_deferred = h[kStDeferred];
+    out->tiles_table = h[kStTiles];
     return SVR_OK;
 }
 

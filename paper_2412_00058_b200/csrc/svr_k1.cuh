@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         if (n_px > oob + 16ull * def) atomicAdd(&ta.stats[kStInserted], n_px - oob - 16ull * def);
         if (oob) atomicAdd(&ta.stats[kStOob], oob);
         if (def) atomicAdd(&ta.stats[kStDeferred], def);
+        if (t1 > t0) atomicAdd(&ta.stats[kStTiles], (ull)(t1 - t0));
     }
 }
 
