@@ -516,7 +516,7 @@ def run_ours(args):
         # ---- per-frame incremental latency (insert -> fill(box+1) -> render(box)), rank-local:
         # the product path is svr_frame_step (one CUDA-graph replay per frame); the per-call
         # sequence of the same kernels is timed beside it
-        def frame_latency(nl, first, graph):
+        def frame_latency(nl, first, graph, src=None):
             le = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
             wall = []
             for j in range(nl):
@@ -525,7 +525,7 @@ def run_ours(args):
                 w = time.perf_counter()
                 le[j][0].record(stream)
                 if graph:
-                    grid.frame_step(frames[k], poses[k:k + 1], wl.calib, fill_r, rp)
+                    grid.frame_step((frames if src is None else src)[k], poses[k:k + 1], wl.calib, fill_r, rp)
                 else:
                     grid.insert_frames(frames[k], poses[k:k + 1], wl.calib)
                     b = boxes[int(mine[k])]
@@ -541,10 +541,22 @@ def run_ours(args):
         mid = max(0, n_my // 2 - nl // 2)
         lat_dev, lat_wall = [], []
         lat_dev_c, lat_wall_c = [], []
+        lat_dev_h, lat_wall_h = [], []
+        cap0 = grid.stats()["graph_captures"]
         if nl:
             frame_latency(3, max(mid - 3, 0), True)  # graph capture + warm-up, untimed
+            cap0 = grid.stats()["graph_captures"]
             lat_dev, lat_wall = frame_latency(nl, mid, True)
             lat_dev_c, lat_wall_c = frame_latency(nl, mid, False)
+            # the real system's frame arrives in pinned host memory: its H2D is inside the step
+            lat_dev_h, lat_wall_h = frame_latency(nl, mid, True, frames_host)
+        recaptures = grid.stats()["graph_captures"] - cap0
+        if world > 1:  # every rank's frames: the union's percentiles, max over ranks
+            allv = [None] * world
+            dist.all_gather_object(allv, (lat_dev, lat_wall, lat_dev_c, lat_wall_c, lat_dev_h, lat_wall_h, recaptures))
+            lat_dev, lat_wall, lat_dev_c, lat_wall_c, lat_dev_h, lat_wall_h = (
+                sum((a[i] for a in allv), []) for i in range(6))
+            recaptures = sum(a[6] for a in allv)
 
     stats = grid.stats()
     hbm, peak_src = _peaks()
@@ -554,7 +566,7 @@ def run_ours(args):
     e2e_value = total_px * e2e_steps / e2e_s / 1e9
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:  # beside every N
         idx, cf = sample_frames(wl, args.cpu_every)
         nth = _ncpu()
         kind, times, px = cpu_reference(wl, cf, wl.poses[idx], nth, min_seconds=args.cpu_seconds,
@@ -632,7 +644,15 @@ def run_ours(args):
                        "device_max": max(lat_dev) if lat_dev else None, "wall_p50": pct(lat_wall, 0.5),
                        "wall_p95": pct(lat_wall, 0.95), "wall_max": max(lat_wall) if lat_wall else None,
                        "what": "one frame: insert + fill(conservative box+1) + render(box) as one CUDA-graph "
-                               "replay (svr_frame_step), rank-local",
+                               "replay (svr_frame_step) from a device-resident frame; at N > 1 every "
+                               "rank's frames (percentiles over their union), the render storing its "
+                               "owned rows into every rank's image (fused gather)",
+                       "graph_recaptures": int(recaptures),
+                       "pinned_host": {"device_p50": pct(lat_dev_h, 0.5), "device_p95": pct(lat_dev_h, 0.95),
+                                       "device_max": max(lat_dev_h) if lat_dev_h else None,
+                                       "wall_p50": pct(lat_wall_h, 0.5), "wall_p95": pct(lat_wall_h, 0.95),
+                                       "what": "the same step from a pinned host frame: its 240 KB H2D "
+                                               "copy enqueued ahead of the graph, inside the timing"},
                        "per_call": {"device_p50": pct(lat_dev_c, 0.5), "device_p95": pct(lat_dev_c, 0.95),
                                     "wall_p50": pct(lat_wall_c, 0.5),
                                     "what": "the same kernels launched call by call"}},
@@ -683,7 +703,36 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world is None:
+        return spawn_ranks(args.gpus)
+    if world is not None and int(world) != args.gpus:
+        print(json.dumps({"error": "--gpus %d but WORLD_SIZE=%s" % (args.gpus, world)}), flush=True)
+        return 2
     return run_ours(args)
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: re-exec under torch.distributed.run with one rank
+    per GPU on this node (rendezvous on 127.0.0.1), failing loudly when fewer GPUs are visible."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": "--gpus %d but only %d CUDA device(s) visible" % (n, have)}), flush=True)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL's communicator init lines (nranks per communicator) stay visible, on stderr
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

@@ -100,6 +100,7 @@ typedef struct svr_stats {
     uint64_t kernel_launches;  /* kernels this handle launched (all kinds) */
     uint64_t chunks_deferred;  /* 16-px chunks sent to the exact per-pixel pass (ties, edges) */
     uint64_t tiles_table;      /* B-scan tiles inserted through the shared-table kernel (K1) */
+    uint64_t graph_captures;   /* svr_frame_step graph (re-)captures */
 } svr_stats;
 
 /* Depth-band coronal render (BASELINE cfg4).  Depth axis = grid y, depth(y) = y*voxel_mm.
@@ -201,6 +202,34 @@ int svr_render_coronal_boxes(svr_volume* vol, const svr_box* dirty, int32_t n, i
  * the ranks (e.g. a symmetric-memory barrier) before reading. */
 int svr_set_gather_targets(svr_volume* vol, void* const* images, int32_t n, int32_t own_z0,
                            int32_t own_z1);
+/* ---------------------------------------------------------------- z-slab sharding ---- */
+/* A z-slab sharded PNN / trilinear volume over ndev devices, for C / C++ callers
+ * driving several GPUs from one thread: slab r (svr_plan_slabs) lives on devices[r] (devices may
+ * repeat) with `ghost` = fill radius + render median radius extra planes per side; frames are
+ * routed to the slabs their conservative box meets; the coronal image [2][nz][nx] is gathered on
+ * devices[0] by the slabs' renders themselves (peer stores over NVLink).  Bit-identical to one
+ * unsharded volume. */
+typedef struct svr_sharded svr_sharded;
+int svr_sharded_create(const svr_grid_desc* desc, const int32_t* devices, int32_t ndev,
+                       int32_t ghost, svr_sharded** out);
+int svr_sharded_destroy(svr_sharded* s);
+/* slab r's volume handle (for readout) and its owned / stored global planes [z0, z1) */
+int svr_sharded_slab(const svr_sharded* s, int32_t r, svr_volume** vol, int32_t* own_z0,
+                     int32_t* own_z1, int32_t* alloc_z0, int32_t* alloc_z1);
+/* batched insert routed to the slabs (asynchronous per slab); routed_out[r] (may be NULL) =
+ * frames slab r took.  Frames in host memory or device memory visible to every device. */
+int svr_sharded_insert_frames(svr_sharded* s, const uint8_t* px, int64_t row_pitch,
+                              int64_t frame_stride, int32_t w, int32_t h, int32_t nframes,
+                              const svr_rigid* poses, const svr_calib* calib, int32_t skip_zero,
+                              int32_t* routed_out);
+/* fill (dirty region + radius) and depth-band render of every slab's dirty columns since the
+ * last call; the renders store their owned rows into the gathered image */
+int svr_sharded_fill_render(svr_sharded* s, int32_t fill_radius, int32_t fill_mode,
+                            const svr_render_params* params);
+int svr_sharded_sync(svr_sharded* s);
+/* gathered image: nz rows x nx (mean, max f32; depth i32); outputs may be NULL; synchronises */
+int svr_sharded_read_coronal(svr_sharded* s, float* mean_out, float* max_out, int32_t* depth_out);
+
 /* Copy rendered rows z in [z0,z1] (global, inside the slab) as nx-wide row-major images. */
 int svr_read_coronal(svr_volume* vol, int32_t z0, int32_t z1, float* mean_out, float* max_out,
                      int32_t* depth_out);

@@ -213,6 +213,75 @@ private:
     svr_grid_desc desc_{};
 };
 
+// z-slab sharded volume over several devices driven from one thread (svr_sharded_*, SURVEY.md
+// §8e): routing, ghost planes and the fused coronal gather happen inside; bit-identical to one
+// VoxelGrid.  devices may repeat (several slabs on one GPU).
+class ShardedVolume {
+public:
+    ShardedVolume(const GridConfig& c, const std::vector<int32_t>& devices, int ghost = 3) {
+        svr_grid_desc d{};
+        d.nx = c.nx;
+        d.ny = c.ny;
+        d.nz = c.nz;
+        d.accum = c.accum;
+        d.voxel_mm = c.voxel_mm;
+        for (int k = 0; k < 3; ++k) d.origin_mm[k] = c.origin_mm[k];
+        d.z_begin = 0;
+        d.z_end = c.nz;
+        check(svr_sharded_create(&d, devices.data(), (int32_t)devices.size(), ghost, &h_));
+        desc_ = d;
+        n_ = (int)devices.size();
+    }
+    ~ShardedVolume() { svr_sharded_destroy(h_); }
+    ShardedVolume(const ShardedVolume&) = delete;
+    ShardedVolume& operator=(const ShardedVolume&) = delete;
+
+    int slabs() const { return n_; }
+    // (handle, owned [z0, z1), stored [z0, z1)) of slab r
+    svr_volume* slab(int r, int32_t* own0 = nullptr, int32_t* own1 = nullptr) const {
+        svr_volume* v = nullptr;
+        check(svr_sharded_slab(h_, r, &v, own0, own1, nullptr, nullptr));
+        return v;
+    }
+    // batched insert routed to the slabs; returns the frames each slab took
+    std::vector<int32_t> insert_frames(const uint8_t* px, int64_t row_pitch, int64_t frame_stride, int w,
+                                       int h, int n, const svr_rigid* poses, const svr_calib& calib,
+                                       bool skip_zero = false) {
+        std::vector<int32_t> routed((size_t)n_);
+        check(svr_sharded_insert_frames(h_, px, row_pitch, frame_stride, w, h, n, poses, &calib,
+                                        skip_zero ? 1 : 0, routed.data()));
+        return routed;
+    }
+    void fill_render(const svr_render_params& p, int fill_radius = 1, int fill_mode = SVR_FILL_MEAN) {
+        check(svr_sharded_fill_render(h_, fill_radius, fill_mode, &p));
+    }
+    void read_coronal(std::vector<float>& mean, std::vector<float>& maxv, std::vector<int32_t>& depth) {
+        const size_t n = (size_t)desc_.nx * desc_.nz;
+        mean.resize(n);
+        maxv.resize(n);
+        depth.resize(n);
+        check(svr_sharded_read_coronal(h_, mean.data(), maxv.data(), depth.data()));
+    }
+    // owned planes of every slab, concatenated in z: the whole grid's accumulators
+    void accumulators(std::vector<uint32_t>& sum, std::vector<uint16_t>& count) {
+        const size_t plane = (size_t)desc_.nx * desc_.ny;
+        sum.assign(plane * desc_.nz, 0);
+        count.assign(plane * desc_.nz, 0);
+        for (int r = 0; r < n_; ++r) {
+            int32_t o0 = 0, o1 = 0;
+            svr_volume* v = slab(r, &o0, &o1);
+            if (o1 <= o0) continue;
+            svr_box b{0, 0, o0, desc_.nx - 1, desc_.ny - 1, o1 - 1};
+            check(svr_read_accumulators(v, &b, sum.data() + plane * o0, count.data() + plane * o0));
+        }
+    }
+
+private:
+    svr_sharded* h_ = nullptr;
+    svr_grid_desc desc_{};
+    int n_ = 0;
+};
+
 inline DirtyRegion insert_frame(VoxelGrid& g, const uint8_t* px, int w, int h, const svr_rigid& pose,
                                 const svr_calib& calib, bool skip_zero = false) {
     return g.insert_frame(px, w, w, h, pose, calib, skip_zero);

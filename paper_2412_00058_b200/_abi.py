@@ -66,7 +66,7 @@ class Stats(C.Structure):
                 ("pixels_oob", C.c_uint64), ("pixels_skipped_zero", C.c_uint64),
                 ("pixels_saturated", C.c_uint64), ("exact_fallbacks", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("chunks_deferred", C.c_uint64),
-                ("tiles_table", C.c_uint64)]
+                ("tiles_table", C.c_uint64), ("graph_captures", C.c_uint64)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
@@ -140,6 +140,14 @@ SIGNATURES = {
     "svr_smooth_depths": (C.c_int, [P, P, I32, I32, P]),
     "svr_bone_contour": (C.c_int, [P, I64, I64, I32, I32, I32, D, I32, I32, D, P, P, P, P, C.c_int, P]),
     "svr_apply_cut": (C.c_int, [P, I64, I64, I32, I32, I32, P, P, C.c_int, P]),
+    "svr_sharded_create": (C.c_int, [PG, C.POINTER(I32), I32, I32, C.POINTER(P)]),
+    "svr_sharded_destroy": (C.c_int, [P]),
+    "svr_sharded_slab": (C.c_int, [P, I32, C.POINTER(P), C.POINTER(I32), C.POINTER(I32), C.POINTER(I32),
+                                   C.POINTER(I32)]),
+    "svr_sharded_insert_frames": (C.c_int, [P, P, I64, I64, I32, I32, I32, PR, PC, I32, C.POINTER(I32)]),
+    "svr_sharded_fill_render": (C.c_int, [P, I32, I32, C.POINTER(RenderParams)]),
+    "svr_sharded_sync": (C.c_int, [P]),
+    "svr_sharded_read_coronal": (C.c_int, [P, P, P, P]),
 }
 
 _lib = None

@@ -2051,6 +2051,7 @@ extern "C" int svr_get_stats(svr_volume* v, svr_stats* out) {
     out->kernel_launches = v->launches;
     out->chunks_deferred = h[kStDeferred];
     out->tiles_table = h[kStTiles];
+    out->graph_captures = v->fg.captures;
     return SVR_OK;
 }
 

@@ -62,6 +62,82 @@ def union_box(boxes, idx, alloc) -> _abi.Box:
                     max(b.y1 for b in bs), z1)
 
 
+class ShardedGrid:
+    """z-slab sharded volume driven from one process over several devices through the C-ABI
+    (svr_sharded_*): the path a C / C++ caller takes without torch.distributed.  devices may
+    repeat (several slabs on one GPU).  Results equal one unsharded VoxelGrid bit for bit."""
+
+    def __init__(self, dims, voxel_mm, origin=(0.0, 0.0, 0.0), devices=(0,), ghost=3,
+                 accum=_abi.ACC_PNN):
+        d = _abi.GridDesc()
+        d.nx, d.ny, d.nz = (int(v) for v in dims)
+        d.accum = accum
+        d.voxel_mm = float(voxel_mm)
+        for k in range(3):
+            d.origin_mm[k] = float(origin[k])
+        d.z_begin, d.z_end = 0, d.nz
+        self.desc = d
+        devs = (_abi.I32 * len(devices))(*devices)
+        h = C.c_void_p()
+        _abi.check(_abi.lib().svr_sharded_create(C.byref(self.desc), devs, len(devices), ghost, C.byref(h)))
+        self._h = h
+        self.n = len(devices)
+
+    def close(self):
+        if self._h:
+            _abi.lib().svr_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def slab(self, r):
+        """(volume handle, owned (z0, z1), stored (z0, z1)) of slab r."""
+        v = C.c_void_p()
+        o0, o1, a0, a1 = (_abi.I32() for _ in range(4))
+        _abi.check(_abi.lib().svr_sharded_slab(self._h, r, C.byref(v), C.byref(o0), C.byref(o1),
+                                               C.byref(a0), C.byref(a1)))
+        return v, (o0.value, o1.value), (a0.value, a1.value)
+
+    def insert_frames(self, frames, poses, calib):
+        from .reconstruct import _frames_view
+        keep, p, pitch, stride, n, h, w = _frames_view(frames)
+        pa = _abi.rigid_array(poses)
+        routed = (_abi.I32 * self.n)()
+        _abi.check(_abi.lib().svr_sharded_insert_frames(self._h, p, pitch, stride, w, h, n,
+                                                        _abi.rigid_ptr(pa), C.byref(calib), 0, routed))
+        _abi.check(_abi.lib().svr_sharded_sync(self._h))
+        del keep
+        return list(routed)
+
+    def fill_render(self, fill_radius, fill_mode, params):
+        _abi.check(_abi.lib().svr_sharded_fill_render(self._h, fill_radius, fill_mode, C.byref(params)))
+
+    def read_coronal(self):
+        nz, nx = self.desc.nz, self.desc.nx
+        mean = np.zeros((nz, nx), np.float32)
+        mx = np.zeros((nz, nx), np.float32)
+        dep = np.full((nz, nx), -1, np.int32)
+        _abi.check(_abi.lib().svr_sharded_read_coronal(self._h, mean.ctypes.data, mx.ctypes.data,
+                                                       dep.ctypes.data))
+        return mean, mx, dep
+
+    def accumulators(self, r):
+        """Owned planes of slab r: (sum u32, count u16) [z, y, x]."""
+        v, own, _ = self.slab(r)
+        nx, ny = self.desc.nx, self.desc.ny
+        nz = own[1] - own[0]
+        s = np.zeros((nz, ny, nx), np.uint32)
+        c = np.zeros((nz, ny, nx), np.uint16)
+        if nz:
+            b = _abi.Box(0, 0, own[0], nx - 1, ny - 1, own[1] - 1)
+            _abi.check(_abi.lib().svr_read_accumulators(v, C.byref(b), s.ctypes.data, c.ctypes.data))
+        return s, c
+
+
 def gather_rows(local, slab: Slab, slabs, dist):
     """All-gather each rank's owned coronal rows (torch tensor [owned_rows, ...]) into the full
     image [nz, ...] (padded equal strips, one all_gather_into_tensor).  Returns the image."""

@@ -6,6 +6,7 @@
 // Built with -DSPINEVOL_B200_REFERENCE_TYPES (+ the reference's include dir) it takes the
 // reference's own spinevol::Image8 / RigidTransform / ImageCalibration.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -131,14 +132,54 @@ static int run(const char* in, const char* out) {
     return o ? 0 : 11;
 }
 
+// Same input, reconstructed by a z-slab sharded volume of `nslab` slabs (all on device 0 here;
+// the same code drives one slab per GPU): OUT = u32 sum[], u16 count[], f32 mean[], f32 max[],
+// i32 depth[] (coronal image nz x nx, cfg4 render parameters).
+static int shard(const char* in, const char* out, int nslab) {
+    std::ifstream f(in, std::ios::binary);
+    int32_t hdr[6];
+    double vox, org[3];
+    svr_calib calib{};
+    f.read((char*)hdr, sizeof hdr);
+    f.read((char*)&vox, 8);
+    f.read((char*)org, 24);
+    f.read((char*)&calib, sizeof calib);
+    const int n = hdr[3], w = hdr[4], h = hdr[5];
+    std::vector<svr_rigid> poses((size_t)n);
+    std::vector<uint8_t> px((size_t)n * w * h);
+    f.read((char*)poses.data(), sizeof(svr_rigid) * n);
+    f.read((char*)px.data(), (std::streamsize)px.size());
+    if (!f) return 10;
+    sb::GridConfig gc{hdr[0], hdr[1], hdr[2], vox, {org[0], org[1], org[2]}};
+    svr_render_params rp{15.0, 60.0, 5.0, 2.0, 2, SVR_FILL_MEAN};
+    sb::ShardedVolume sv(gc, std::vector<int32_t>((size_t)nslab, 0), 1 + rp.median_radius);
+    sv.insert_frames(px.data(), w, (int64_t)w * h, w, h, n, poses.data(), calib);
+    sv.fill_render(rp, 1, SVR_FILL_MEAN);
+    std::vector<uint32_t> sum;
+    std::vector<uint16_t> cnt;
+    sv.accumulators(sum, cnt);
+    std::vector<float> mean, maxv;
+    std::vector<int32_t> depth;
+    sv.read_coronal(mean, maxv, depth);
+    std::ofstream o(out, std::ios::binary);
+    o.write((char*)sum.data(), (std::streamsize)(sum.size() * 4));
+    o.write((char*)cnt.data(), (std::streamsize)(cnt.size() * 2));
+    o.write((char*)mean.data(), (std::streamsize)(mean.size() * 4));
+    o.write((char*)maxv.data(), (std::streamsize)(maxv.size() * 4));
+    o.write((char*)depth.data(), (std::streamsize)(depth.size() * 4));
+    std::puts("shard ok");
+    return o ? 0 : 11;
+}
+
 int main(int argc, char** argv) {
     try {
         if (argc >= 2 && !std::strcmp(argv[1], "host")) return host_checks();
         if (argc >= 4 && !std::strcmp(argv[1], "run")) return run(argv[2], argv[3]);
+        if (argc >= 5 && !std::strcmp(argv[1], "shard")) return shard(argv[2], argv[3], std::atoi(argv[4]));
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 20;
     }
-    std::fprintf(stderr, "usage: wrapper_demo host | run IN OUT\n");
+    std::fprintf(stderr, "usage: wrapper_demo host | run IN OUT | shard IN OUT NSLAB\n");
     return 2;
 }
