@@ -71,6 +71,7 @@ def lib():
         L.orc_bone_contour.restype = C.c_int32
         L.orc_smooth_depths.argtypes = [P, P, C.c_int32, C.c_int32, P]
         L.orc_insert_trilinear.argtypes = [PG, P, C.c_int64, C.c_int32, C.c_int32, PR, PC, C.c_int32]
+        L.orc_insert_trilinear_f64.argtypes = [PG, P, C.c_int64, C.c_int32, C.c_int32, PR, PC, C.c_int32, P, P]
         _lib = L
     return _lib
 
@@ -179,6 +180,19 @@ class OracleGrid:
         pa = rigid_array(pose)
         lib().orc_insert_trilinear(C.byref(self.g), frame.ctypes.data, w, w, h, rigid_ptr(pa),
                                    C.byref(calib), int(skip_zero))
+
+    def insert_trilinear_f64(self, frames, poses, calib, skip_zero=False):
+        """Trilinear splat summed in fp64 (self.wsum64 / self.weight64): the parity reference."""
+        if getattr(self, "wsum64", None) is None:
+            self.wsum64 = np.zeros(self.sum.shape, np.float64)
+            self.weight64 = np.zeros(self.sum.shape, np.float64)
+        pa = rigid_array(poses)
+        for k in range(len(pa)):
+            f = np.ascontiguousarray(frames[k], dtype=np.uint8)
+            h, w = f.shape
+            lib().orc_insert_trilinear_f64(C.byref(self.g), f.ctypes.data, w, w, h, rigid_ptr(pa[k:k + 1]),
+                                           C.byref(calib), int(skip_zero), self.wsum64.ctypes.data,
+                                           self.weight64.ctypes.data)
 
     def fill_holes(self, region=None, mode=0, radius=1) -> int:
         b = None if region is None else C.byref(region if isinstance(region, Box) else Box(*region))

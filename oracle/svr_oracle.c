@@ -422,6 +422,11 @@ int64_t orc_fill_holes(orc_grid* g, const svr_box* region, int32_t mode, int32_t
 
 /* f32 value of a voxel for rendering; returns 0 when the voxel is undefined. */
 static inline int voxel_f(const orc_grid* g, int64_t lin, int32_t fill_mode, float* f) {
+    if (g->weight) { /* trilinear volume (BASELINE cfg5): f = wsum / weight, defined iff weight > 0 */
+        if (!(g->weight[lin] > 0.0f)) return 0;
+        *f = g->wsum[lin] / g->weight[lin];
+        return 1;
+    }
     uint32_t c = g->count[lin];
     if (c) {
         *f = (float)voxel_value(g->sum[lin], c);
@@ -605,8 +610,26 @@ void orc_coronal_projection(const orc_grid* g, int32_t mode, int32_t axis, int32
 /* Trilinear splat (BASELINE cfg5): u = (p - origin)/voxel, i0 = floor(u), f = u - i0; the
  * 8 corners (clipped to the slab) get w = prod(f or 1-f); wsum += w*px, weight += w.
  * Accumulated in f32 in row-major pixel order (the tolerance test absorbs order). */
+/* ws64 / wt64 non-NULL: accumulate the same fp32-rounded contributions in fp64 instead (the
+ * parity reference: the GPU differs from it only by the rounding of its fp32 sums). */
+static int trilinear_impl(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
+                          const svr_rigid* pose, const svr_calib* c, int32_t skip_zero, double* ws64,
+                          double* wt64);
+
 int orc_insert_trilinear(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
                          const svr_rigid* pose, const svr_calib* c, int32_t skip_zero) {
+    return trilinear_impl(g, px, pitch, w, h, pose, c, skip_zero, NULL, NULL);
+}
+
+int orc_insert_trilinear_f64(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
+                             const svr_rigid* pose, const svr_calib* c, int32_t skip_zero,
+                             double* wsum64, double* weight64) {
+    return trilinear_impl(g, px, pitch, w, h, pose, c, skip_zero, wsum64, weight64);
+}
+
+static int trilinear_impl(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
+                          const svr_rigid* pose, const svr_calib* c, int32_t skip_zero, double* ws64,
+                          double* wt64) {
     if (w != c->crop_w || h != c->crop_h) return SVR_E_INVALID;
     double* fs = NULL;
     double* fc = NULL;
@@ -640,8 +663,13 @@ int orc_insert_trilinear(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t 
                 double wt = ((k & 1) ? f[0] : 1.0 - f[0]) * (((k >> 1) & 1) ? f[1] : 1.0 - f[1]) *
                             (((k >> 2) & 1) ? f[2] : 1.0 - f[2]);
                 int64_t lin = (((int64_t)iz - g->z_begin) * g->ny + (int64_t)iy) * g->nx + (int64_t)ix;
-                g->wsum[lin] += (float)(wt * v);
-                g->weight[lin] += (float)wt;
+                if (ws64) {
+                    ws64[lin] += (double)(float)(wt * v);
+                    wt64[lin] += (double)(float)wt;
+                } else {
+                    g->wsum[lin] += (float)(wt * v);
+                    g->weight[lin] += (float)wt;
+                }
                 hit = 1;
             }
             if (hit)

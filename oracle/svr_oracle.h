@@ -75,6 +75,10 @@ void orc_coronal_projection(const orc_grid* g, int32_t mode, int32_t depth_axis,
 /* trilinear (cfg5) */
 int orc_insert_trilinear(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
                          const svr_rigid* pose, const svr_calib* calib, int32_t skip_zero);
+/* same contributions, summed in fp64 into wsum64 / weight64 (slab-sized arrays) */
+int orc_insert_trilinear_f64(orc_grid* g, const uint8_t* px, int64_t pitch, int32_t w, int32_t h,
+                             const svr_rigid* pose, const svr_calib* calib, int32_t skip_zero,
+                             double* wsum64, double* weight64);
 
 /* segment (SPEC.md segment module; the reference implements none of it: parity unpinned
  * except median_lower, core.hpp:93-99, which these use) */

@@ -818,8 +818,12 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
             if (e == cudaSuccess) e = cudaMalloc(&v->r_mdepth, sizeof(int) * ncol);
             if (e == cudaSuccess) e = cudaMalloc(&v->r_mean, sizeof(float) * ncol);
             if (e == cudaSuccess) e = cudaMalloc(&v->r_max, sizeof(float) * ncol);
-        } else {
+        } else {  // trilinear: the f32 pair per voxel + the render layer (BASELINE cfg5)
             e = cudaMalloc(&v->tri, sizeof(float2) * v->nvox);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_depth, sizeof(int) * ncol);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_mdepth, sizeof(int) * ncol);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_mean, sizeof(float) * ncol);
+            if (e == cudaSuccess) e = cudaMalloc(&v->r_max, sizeof(float) * ncol);
         }
     }
     if (e == cudaSuccess) {  // the fill's reciprocal table (per device; idempotent)
@@ -1761,7 +1765,7 @@ static long long tile_cols(std::vector<ColTiles>& ct, int cols_per_cta = 128) {
 
 static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill_radius,
                         const svr_render_params* p) {
-    if (!v->acc) return fail(SVR_E_INVALID, "render needs a PNN volume");
+    if (!v->acc && !v->tri) return fail(SVR_E_INVALID, "render needs a volume");
     if (!p) return fail(SVR_E_INVALID, "render params NULL");
     if (p->median_radius < 0 || p->median_radius > 2)
         return fail(SVR_E_INVALID, "median_radius must be 0, 1 or 2");
@@ -1786,6 +1790,19 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
     const ColTiles* ddt = (const ColTiles*)d;
     const ColTiles* dmt = ddt + dt.size();
     const GridDev g = dev_grid(v->d);
+    if (v->tri) {  // trilinear volume: f = wsum / weight, no fill layer
+        k_depth<4, true><<<grid_1d(nd), 128, 0, v->stream>>>(nullptr, nullptr, g, ddt, (int)dt.size(), ylo,
+                                                              yhi, p->fill_mode, v->r_depth, v->tri);
+        v->launches++;
+        CKL();
+        k_band<true><<<grid_1d(nm), 128, 0, v->stream>>>(nullptr, nullptr, g, dmt, (int)mt.size(),
+                                                         p->median_radius, above, below, p->fill_mode,
+                                                         v->r_depth, v->r_mdepth, v->r_mean, v->r_max,
+                                                         v->gt, v->tri);
+        v->launches++;
+        CKL();
+        return SVR_OK;
+    }
     if (v->depth_seg == 8)
         k_depth<8><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
                                                         p->fill_mode, v->r_depth);
@@ -1797,7 +1814,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
                                                         p->fill_mode, v->r_depth);
     v->launches++;
     CKL();
-    k_band<<<grid_1d(nm), 128, 0, v->stream>>>(v->acc, v->fill, g, dmt, (int)mt.size(), p->median_radius,
+    k_band<false><<<grid_1d(nm), 128, 0, v->stream>>>(v->acc, v->fill, g, dmt, (int)mt.size(), p->median_radius,
                                                 above, below, p->fill_mode, v->r_depth, v->r_mdepth,
                                                 v->r_mean, v->r_max, v->gt);
     v->launches++;
@@ -1836,7 +1853,7 @@ extern "C" int svr_read_coronal_async(svr_volume* v, int32_t z0, int32_t z1, flo
 static int read_coronal(svr_volume* v, int32_t z0, int32_t z1, float* mean, float* maxv, int32_t* depth,
                         bool sync) {
     VOL_CHECK(v);
-    if (!v->acc) return fail(SVR_E_INVALID, "render needs a PNN volume");
+    if (!v->r_mean) return fail(SVR_E_INVALID, "volume has no render layer");
     if (z0 < v->d.z_begin || z1 >= v->d.z_end || z0 > z1)
         return fail(SVR_E_INVALID, "rows [%d,%d] outside slab [%d,%d)", z0, z1, v->d.z_begin, v->d.z_end);
     const size_t off = (size_t)(z0 - v->d.z_begin) * v->d.nx, cnt = (size_t)(z1 - z0 + 1) * v->d.nx;
@@ -2166,7 +2183,7 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
         k_fill_warp<2, 1, 8, false><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, nullptr);
         k_depth<8><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, dt, 1, ylo, yhi,
                                                                   p.fill_mode, v->r_depth);
-        k_band<<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, mt, 1, p.median_radius, above,
+        k_band<false><<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, mt, 1, p.median_radius, above,
                                                              below, p.fill_mode, v->r_depth, v->r_mdepth,
                                                              v->r_mean, v->r_max, v->gt);
     }

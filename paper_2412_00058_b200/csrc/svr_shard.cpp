@@ -27,7 +27,7 @@ struct svr_sharded {
     std::vector<svr_volume*> vol;
     std::vector<int32_t> ob, oe, ab, ae;
     std::vector<svr_box> dirty;  // per slab: union of routed frames' boxes since the last render
-    float* img = nullptr;        // [2][nz][nx] on dev[0] (PNN volumes)
+    float* img = nullptr;        // [2][nz][nx] on dev[0]
     svr_render_params last{};
 };
 
@@ -98,7 +98,7 @@ extern "C" int svr_sharded_create(const svr_grid_desc* desc, const int32_t* devi
             return e;
         }
     }
-    if (desc->accum == SVR_ACC_PNN) {
+    {
         const size_t bytes = 2ull * (size_t)desc->nz * (size_t)desc->nx * sizeof(float);
         cudaError_t e = cudaSetDevice(devices[0]);
         if (e == cudaSuccess) e = cudaMalloc(&s->img, bytes);
@@ -197,7 +197,6 @@ extern "C" int svr_sharded_insert_frames(svr_sharded* s, const uint8_t* px, int6
 extern "C" int svr_sharded_fill_render(svr_sharded* s, int32_t fill_radius, int32_t fill_mode,
                                        const svr_render_params* params) {
     if (!s) return svr_fail(SVR_E_INVALID, "NULL sharded volume");
-    if (s->d.accum != SVR_ACC_PNN) return svr_fail(SVR_E_INVALID, "fill / render need a PNN volume");
     if (!params) return svr_fail(SVR_E_INVALID, "NULL render params");
     for (int r = 0; r < s->n; ++r) {
         const svr_box u = s->dirty[(size_t)r];
@@ -210,8 +209,10 @@ extern "C" int svr_sharded_fill_render(svr_sharded* s, int32_t fill_radius, int3
         f.x1 = std::min(f.x1, s->d.nx - 1);
         f.y1 = std::min(f.y1, s->d.ny - 1);
         f.z1 = std::min(f.z1, s->ae[r] - 1);
-        if (int e = svr_fill_holes(s->vol[r], &f, fill_mode, fill_radius, nullptr)) return e;
-        if (int e = svr_render_coronal(s->vol[r], &u, fill_radius, params)) return e;
+        const bool pnn = s->d.accum == SVR_ACC_PNN;  // (trilinear volumes have no hole fill)
+        if (pnn)
+            if (int e = svr_fill_holes(s->vol[r], &f, fill_mode, fill_radius, nullptr)) return e;
+        if (int e = svr_render_coronal(s->vol[r], &u, pnn ? fill_radius : 0, params)) return e;
         s->dirty[(size_t)r] = svr_box{1, 1, 1, 0, 0, 0};
     }
     s->last = *params;
@@ -230,7 +231,6 @@ extern "C" int svr_sharded_sync(svr_sharded* s) {
 extern "C" int svr_sharded_read_coronal(svr_sharded* s, float* mean_out, float* max_out,
                                         int32_t* depth_out) {
     if (!s) return svr_fail(SVR_E_INVALID, "NULL sharded volume");
-    if (!s->img) return svr_fail(SVR_E_INVALID, "render needs a PNN volume");
     if (int e = svr_sharded_sync(s)) return e;
     const size_t plane = (size_t)s->d.nz * (size_t)s->d.nx;
     CKR(cudaSetDevice(s->dev[0]));

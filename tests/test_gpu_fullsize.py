@@ -206,3 +206,46 @@ def test_frame_step_padded_pitch_device_frame():
     ref = O.OracleGrid.for_workload(wl)
     ref.insert_frames(frames, wl.poses, wl.calib)
     _assert_acc(a, ref, "pitched frame_step")
+
+
+def test_cfg5_trilinear_gigabyte_slab_vs_oracle():
+    """cfg5 (0.08 mm, 2000 x 1000 x 7500 grid) on a 64-plane z-slab (2000 x 1000 x 64 voxels,
+    1.02 GB of f32 pairs) with every frame whose box meets it: weights and weighted sums within
+    1e-5 relative of the oracle's fp64 sum of the same contributions (no absolute floor: both
+    take u from the fp64 chain, only the GPU's fp32 accumulation order differs); then the
+    depth-band render of the slab equals the oracle's render of the GPU's own f32 volume."""
+    wl = synth.cfg5()
+    z0 = 1200
+    slab = (z0, z0 + 64)
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    idx = sharding.route(boxes, slab)
+    assert 50 < len(idx) < 400
+    import torch
+    dev = torch.empty((len(idx), wl.h, wl.w), dtype=torch.uint8, device="cuda")
+    for i, k in enumerate(idx):
+        synth.synth_frames_device(wl, dev[i:i + 1], int(k), 1)
+    host = dev.cpu().numpy()
+    poses = wl.poses[idx]
+    grid = pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, device=0, z_range=slab, accum=wl.accum)
+    grid.insert_frames(dev, poses, wl.calib)
+    ws, wt = grid.trilinear()
+    assert ws.nbytes + wt.nbytes >= 1.0e9
+    ref = O.OracleGrid.for_workload(wl, z_range=slab)
+    ref.insert_trilinear_f64(host, poses, wl.calib)
+    assert (ref.weight64 > 0).sum() > 10_000_000
+    np.testing.assert_allclose(wt, ref.weight64, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(ws, ref.wsum64, rtol=1e-5, atol=0)
+    st = grid.stats()
+    assert st["pixels_inserted"] + st["pixels_oob"] == len(idx) * wl.w * wl.h
+    # render: the oracle renders the GPU's own f32 volume (same inputs -> same values)
+    rp = synth.render_params(depth_lo_mm=15.0, depth_hi_mm=60.0)
+    grid.render_coronal(None, rp, 0)
+    mean, mx, dep = grid.read_coronal()
+    ref.wsum[...] = ws
+    ref.weight[...] = wt
+    rmean, rmx, rdep = ref.render(rp, fill_radius=0)
+    assert (dep >= 0).sum() > 10000
+    assert np.array_equal(dep, rdep)
+    np.testing.assert_allclose(mean, rmean, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(mx, rmx, rtol=1e-5, atol=0)
+    grid.close()
