@@ -229,10 +229,79 @@ def measure_config(name, steps=3):
         hbm, _ = _peaks()
         out["roofline_frac"] = alg / (ms / 1e3) / 1e9 / hbm
         out["U_mean"] = float(U.mean())
+    else:
+        out.update(trilinear_extras(wl, grid, frames, stream, ms))
     grid.close()
     del frames
     torch.cuda.empty_cache()
     return out
+
+def trilinear_extras(wl, grid, frames, stream, insert_ms, nsample=16, nlat=40):
+    """cfg5 beside its insert: the roofline over W*H + 16*U8 bytes per frame (U8 = distinct corner
+    voxels a frame's 2x2x2 splat touches, counted on a sample of frames), the depth-band render of
+    the whole volume's columns, and per-frame insert + render latency."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2412_00058_b200 import _abi, sharding, synth
+    L = _abi.lib()
+    hbm, _ = _peaks()
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    # U8: each sampled frame alone in a scratch volume covering its box, non-zero weights counted
+    # on the device
+    u8 = []
+    live = [k for k in range(wl.nframes) if not boxes[k].empty()]
+    for k in np.array(live)[np.linspace(0, len(live) - 1, nsample).astype(int)]:
+        b = boxes[int(k)]
+        dims = (b.x1 - b.x0 + 1, b.y1 - b.y0 + 1, b.z1 - b.z0 + 1)
+        org = tuple(wl.origin[i] + wl.voxel_mm * (b.x0, b.y0, b.z0)[i] for i in range(3))
+        import paper_2412_00058_b200 as pkg
+        sg = pkg.VoxelGrid(dims, wl.voxel_mm, org, accum=wl.accum, device=torch.cuda.current_device())
+        sg.insert_frames(frames[k:k + 1], wl.poses[k:k + 1], wl.calib)
+        wt = torch.empty(int(np.prod(dims)), dtype=torch.float32, device="cuda")
+        _abi.check(L.svr_read_trilinear(sg.handle, None, None, C.c_void_p(wt.data_ptr())))
+        u8.append(int(torch.count_nonzero(wt).item()))
+        sg.close()
+        del wt
+    u8m = float(np.mean(u8))
+    alg = wl.nframes * (wl.w * wl.h + 16.0 * u8m)
+    out = {"roofline": {"bound": "hbm", "kernel": "k_insert<trilinear> (K1t)", "unit": "GB/s",
+                        "achieved": alg / (insert_ms / 1e3) / 1e9, "peak": hbm,
+                        "frac": alg / (insert_ms / 1e3) / 1e9 / hbm,
+                        "bytes_model": "W*H + 16*U8 per frame (f32 wsum + weight RMW of each distinct "
+                                       "corner voxel), U8 mean %.0f over %d sampled frames" % (u8m, nsample)},
+           "U8_mean": u8m}
+    rp = synth.render_params()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        grid.render_coronal(None, rp, 0)  # warm
+        a.record(stream)
+        grid.render_coronal(None, rp, 0)
+        b.record(stream)
+        torch.cuda.synchronize()
+    out["render_all_columns_ms"] = a.elapsed_time(b)
+    # per-frame: one frame's splat + the render of its dirty columns (call by call)
+    lat = []
+    mid = live[len(live) // 2]
+    with torch.cuda.stream(stream):
+        for j in range(nlat + 3):
+            k = mid + j
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            grid.insert_frames(frames[k:k + 1], wl.poses[k:k + 1], wl.calib)
+            if not boxes[k].empty():
+                grid.render_coronal(boxes[k], rp, 0)
+            e1.record(stream)
+            e1.synchronize()
+            if j >= 3:
+                lat.append(e0.elapsed_time(e1))
+    lat.sort()
+    out["latency_ms"] = {"frames": len(lat), "device_p50": lat[len(lat) // 2],
+                         "device_p95": lat[int(0.95 * (len(lat) - 1) + 0.5)], "device_max": lat[-1],
+                         "what": "one frame: trilinear splat + depth-band render of its dirty columns"}
+    return out
+
 
 # ---------------------------------------------------------------- our arm
 def slab_shares(wl, frames, boxes, rp, stream, dev, ns=(2, 4, 8), steps=3, nlat=60):
