@@ -147,29 +147,14 @@ struct svr_volume {
     size_t tiles_cap = 0;
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
-    int insert_kernel = 3;      // SVR_INSERT_KERNEL: 3 plane (default), 1 direct, 0 rows, 2 tile
-    int plane_walk = 1;         // SVR_PLANE_WALK: k_pnn_plane pixel walk, 1 step counters, 0 carries
-    int depth_seg = 4;          // SVR_DEPTH_SEG: threads per column in k_depth (4; 8 or 1 A/B)
-    int plane_tw = 4;           // SVR_PLANE_TW: k_pnn_plane tile width in chunks (4, or 6 when it fits)
-    int plane_tw_cur = 4;       // the width chosen for the current insert call
+    int insert_kernel = 3;      // SVR_INSERT_KERNEL=direct: every PNN insert through k_insert (the
+                                // fallback kernel; tests use it to cover it on every geometry)
     int lin_shapes_cur = 0;     // k_pnn_tiles shapes every frame of the current insert call fits
-    int tiles_occ[8] = {};      // k_pnn_tiles resident CTAs per SM, per <shape, box> (lazy)
+    int tiles_occ[8] = {0};     // k_pnn_tiles resident CTAs per SM, per <shape, box> (lazy)
     TileDesc* d_desc = nullptr; // k_pnn_tiles per-tile descriptors
     long long desc_cap = 0;
-    int plane_flush_lin = 1;    // SVR_PLANE_FLUSH: k_pnn_lin table flush, 1 linear over all threads, 0 lane = x
-    int lin_small = 4;          // SVR_LIN_SMALL: launches of <= this many frames use 64-row k_pnn_lin tiles
-    int plane_lin = 1;          // SVR_PLANE_LIN: k_pnn_lin for linear probes (1: 128-row tiles, 2: 64), 0 k_pnn_plane
-    int plane_prefetch = 2;     // SVR_PLANE_PREFETCH: L2 prefetch of each chunk (0 off, 1 both ends, 2 start voxel)
-    bool fill_smem = false;     // SVR_FILL_KERNEL=smem: shared-memory separable fill for r=1
     int num_sms = 148;          // the device's SM count (grid sizing)
-    int fill_zc = 0;            // SVR_FILL_ZC: planes per warp-march in k_fill_warp (8/16/32; 0 = by region size)
     int fill_mode = SVR_FILL_MEAN;  // mode of the latest fill_holes: decodes the fill layer on readout
-    bool fill_tma = false;      // SVR_FILL_KERNEL=tma selects k_fill_tma (opt-in: 0.43 vs 0.385 ms)
-    int fill_tma_zc = 32;       // SVR_FILL_TMA_ZC: planes per CTA in k_fill_tma (16/32)
-    int tmap_state = 0;         // accumulator tensor map: 0 not built, 1 ready, -1 unavailable
-    CUtensorMap tmap;
-    int fill_depth = 1;         // SVR_FILL_DEPTH: planes in flight per warp in k_fill_warp (1/2)
-    int fill_ty = 8;            // SVR_FILL_TY: y rows per warp in k_fill_warp (4/8/12/16)
 };
 
 // ---------------------------------------------------------------- host geometry (exact)
@@ -386,11 +371,6 @@ static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, doubl
         for (int j = 0; j < 3; ++j) fp->M[3 * k + j] = a.Mv[3 * k + j];
     }
     if (!ok) return fail(SVR_E_INVALID, "pose maps the frame too far from the grid (|u| >= 1e8 voxels)");
-    for (int k = 0; k < 3; ++k) {  // k_pnn_lin tile corners: 64 columns x 128 rows
-        const long long c1 = 63ll * fp->Dc[k], r1 = 127ll * fp->Dr[k];
-        fp->tmn[k] = std::min(std::min(0ll, c1), std::min(r1, c1 + r1));
-        fp->tmx[k] = std::max(std::max(0ll, c1), std::max(r1, c1 + r1));
-    }
     fp->pose = pose;
     fp->cal = x.cal;
     fp->g = x.g;
@@ -772,32 +752,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     if (device < 0 || device >= ndev) return fail(SVR_E_INVALID, "device %d out of range", device);
     svr_volume* v = new svr_volume();
     v->d = *desc;
-    if (const char* e = std::getenv("SVR_FILL_KERNEL")) {
-        v->fill_smem = !std::strcmp(e, "smem");
-        v->fill_tma = !std::strcmp(e, "tma");
-    }
-    if (const char* e = std::getenv("SVR_FILL_ZC")) v->fill_zc = std::atoi(e);
-    if (const char* e = std::getenv("SVR_FILL_TMA_ZC")) v->fill_tma_zc = std::atoi(e) == 16 ? 16 : 32;
-    if (const char* e = std::getenv("SVR_FILL_DEPTH")) v->fill_depth = std::atoi(e) == 1 ? 1 : 2;
-    if (const char* e = std::getenv("SVR_FILL_TY")) {
-        const int t = std::atoi(e);
-        v->fill_ty = (t == 4 || t == 12 || t == 16) ? t : 8;
-    }
-    if (const char* e = std::getenv("SVR_PLANE_WALK")) v->plane_walk = std::atoi(e) ? 1 : 0;
-    if (const char* e = std::getenv("SVR_DEPTH_SEG")) {
-        const int sg = std::atoi(e);
-        v->depth_seg = (sg == 1 || sg == 8) ? sg : 4;
-    }
-    if (const char* e = std::getenv("SVR_PLANE_TW")) v->plane_tw = std::atoi(e) == 6 ? 6 : 4;
-    if (const char* e = std::getenv("SVR_PLANE_FLUSH")) v->plane_flush_lin = std::atoi(e) ? 1 : 0;
-    if (const char* e = std::getenv("SVR_LIN_SMALL")) v->lin_small = std::atoi(e);
-    if (const char* e = std::getenv("SVR_PLANE_LIN")) v->plane_lin = std::min(3, std::max(0, std::atoi(e)));
-    if (const char* e = std::getenv("SVR_PLANE_PREFETCH")) v->plane_prefetch = std::min(2, std::max(0, std::atoi(e)));
-    if (const char* e = std::getenv("SVR_INSERT_KERNEL"))
-        v->insert_kernel = !std::strcmp(e, "rows")     ? 0
-                           : !std::strcmp(e, "tile")   ? 2
-                           : !std::strcmp(e, "direct") ? 1
-                                                       : 3;
+    if (const char* e = std::getenv("SVR_INSERT_KERNEL")) v->insert_kernel = !std::strcmp(e, "direct") ? 1 : 3;
 
     v->device = device;
     auto bail = [&](int code) {
@@ -1025,71 +980,6 @@ static bool is_device_ptr(const void* p, bool* pinned) {
     return false;
 }
 
-// Tile-hash insert (k_pnn_tile) applicability for a launch: the packed (count<<20 | sum) slot
-// must not overflow (some pixel pair of every tile lies more than a voxel diagonal apart, so no
-// voxel collects all 4096 pixels of a tile) and tile-local keys must fit 32 bits.
-struct TileShape {
-    int tw, th, ntx, nty;
-};
-
-static bool tile_ok(const svr_volume* v, const DevCalib& cal, int w, int h, TileShape* ts,
-                    int max_tw) {
-    const int cpr = (w + kChunk - 1) / kChunk;
-    ts->tw = std::min(max_tw, cpr);
-    while (256 % ts->tw) --ts->tw;
-    ts->th = 256 / ts->tw;
-    ts->ntx = (cpr + ts->tw - 1) / ts->tw;
-    ts->nty = (h + ts->th - 1) / ts->th;
-    const double diag = std::sqrt(3.0) * v->d.voxel_mm;
-    const double along = (cal.probe == SVR_PROBE_FAN) ? cal.dr : cal.sx;
-    const double across = (cal.probe == SVR_PROBE_FAN) ? 0.0 : cal.sy;
-    const bool spread = (std::min(ts->tw * kChunk, w) - 1) * along > diag ||
-                        (std::min(ts->th, h) - 1) * across > diag;
-    // keys: a tile spans at most its frame's z extent; bound by the slab (conservative)
-    const double slab = (double)v->d.nx * v->d.ny * (double)(v->d.z_end - v->d.z_begin);
-    return spread && slab < 4.0e9;
-}
-
-template <bool kVec, bool kSkip, bool kBox>
-static void launch_tile_t(svr_volume* v, const uint8_t* px, long long pitch, long long fstride,
-                          int w, int h, int n, const FrameParams* fps, const DevCalib& cal,
-                          const TileShape& ts, int* boxes, ull* stats) {
-    const int cpr = (w + kChunk - 1) / kChunk;
-    dim3 grid(ts.ntx * ts.nty, n);
-    k_pnn_tile<kVec, kSkip, kBox><<<grid, 256, 0, v->stream>>>(
-        px, pitch, fstride, w, h, cpr, ts.tw, ts.th, ts.ntx, n, coprime_stride(n), fps, cal,
-        v->d_fan, dev_grid(v->d), v->acc, boxes, stats);
-    v->launches++;
-}
-
-static void launch_tile(svr_volume* v, bool vec, bool skip, bool box, const uint8_t* px,
-                        long long pitch, long long fstride, int w, int h, int n,
-                        const FrameParams* fps, const DevCalib& cal, const TileShape& ts,
-                        int* boxes, ull* stats) {
-#define LT(a, b, c) launch_tile_t<a, b, c>(v, px, pitch, fstride, w, h, n, fps, cal, ts, boxes, stats)
-    if (vec) {
-        if (skip) { if (box) LT(true, true, true); else LT(true, true, false); }
-        else { if (box) LT(true, false, true); else LT(true, false, false); }
-    } else {
-        if (skip) { if (box) LT(false, true, true); else LT(false, true, false); }
-        else { if (box) LT(false, false, true); else LT(false, false, false); }
-    }
-#undef LT
-}
-
-template <bool kVec, bool kBox>
-static void launch_rows_t(svr_volume* v, const uint8_t* px, long long pitch, long long fstride,
-                          int w, int h, int n, const FrameParams* fps, const DevCalib& cal,
-                          int* boxes, ull* stats) {
-    const int cpr = (w + kChunk - 1) / kChunk;
-    const int nstrips = (h + kStripRows - 1) / kStripRows;
-    dim3 grid((nstrips * cpr + 255) / 256, n);
-    k_pnn_rows<kVec, kBox><<<grid, 256, 0, v->stream>>>(px, pitch, fstride, w, h, cpr, nstrips, fps,
-                                                        cal, v->d_fan, dev_grid(v->d), v->acc,
-                                                        boxes, stats);
-    v->launches++;
-}
-
 // per-tile descriptor buffer of k_pnn_tiles (grown outside any graph capture: fg_capture
 // pre-sizes it for one frame)
 static int ensure_desc(svr_volume* v, long long ntiles) {
@@ -1117,6 +1007,8 @@ static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
     v->launches += 2;
     return SVR_OK;
 }
+
+constexpr int kLinSmall = 4;  // launches of <= 4 frames (the per-frame path) prefer 32-column tiles
 
 static int pick_shape(int shapes, int w, int nframes, int small) {
     static const int big_pref[4] = {0, 1, 2, 3}, small_pref[4] = {1, 3, 0, 2};
@@ -1169,21 +1061,26 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                          uint32_t tag, ull* stats) {
     const bool vec = ((uintptr_t)px % 16 == 0) && (pitch % 16 == 0) && (fstride % 16 == 0) &&
                      (w % kChunk == 0);
-    TileShape ts;
-    const bool tile = mode == kModeInsert && v->insert_kernel == 2 && tile_ok(v, cal, w, h, &ts, 8);
-    const bool plane = mode == kModeInsert && v->insert_kernel == 3 && !skip && w >= 4 * kChunk &&
-                       (long long)v->d.nx * v->d.ny < (1ll << 22) && tile_ok(v, cal, w, h, &ts, 4);
-    const bool rows = mode == kModeInsert && v->insert_kernel == 0 && !skip;
-    // k_pnn_tiles reads each row segment with 32-byte loads
+    const bool direct = v->insert_kernel == 1;
+    // linear probes: k_pnn_tiles (reads each row segment with 32-byte loads)
     const bool vec32 = ((uintptr_t)px % 32 == 0) && (pitch % 32 == 0) && (n == 1 || fstride % 32 == 0);
-    const int shape = (mode == kModeInsert && !skip && cal.probe == SVR_PROBE_LINEAR && vec32 &&
-                       v->insert_kernel == 3)
-                          ? pick_shape(v->lin_shapes_cur, w, n, v->lin_small)
+    const int shape = (mode == kModeInsert && !skip && !direct && cal.probe == SVR_PROBE_LINEAR && vec32)
+                          ? pick_shape(v->lin_shapes_cur, w, n, kLinSmall)
                           : -1;
+    // convex fan: k_pnn_plane's 64 x 64-sample tiles (table only where the tile's extent fits) + the
+    // exact pass.  Its packed (count << 20 | sum) slot holds at most 4095 pixels: guaranteed when
+    // every tile has two samples more than a voxel diagonal apart (63 dr > sqrt(3) voxel)
+    const bool fan_plane = mode == kModeInsert && !skip && !direct && cal.probe == SVR_PROBE_FAN &&
+                           w >= 4 * kChunk && (long long)v->d.nx * v->d.ny < (1ll << 22) &&
+                           63.0 * cal.dr > std::sqrt(3.0) * v->d.voxel_mm;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
         const uint8_t* p = px + (long long)k0 * fstride;
         int* bx = boxes ? boxes + 6 * k0 : nullptr;
+        // the deferred-chunk pass is grid-strided over a worklist of a few entries per frame:
+        // a single frame must not pay for launching thousands of idle CTAs
+        const int work_ctas = std::min(4096, std::max(16, 8 * m));
+        const GridDev gd = dev_grid(v->d);
         if (shape >= 0) {
             // k_pnn_tiles defers whole chunks with no overflow path: room for every chunk
             const long long need = std::max<long long>(1ll << 20, (long long)m * h * (w / kChunk));
@@ -1198,8 +1095,6 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             }
             CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
             if (int e = launch_tiles(v, shape, box, p, pitch, fstride, w, h, m, fps + k0, bx, stats)) return e;
-            const int work_ctas = std::min(4096, std::max(16, 8 * m));
-            const GridDev gd = dev_grid(v->d);
             if (box)
                 k_pnn_work<true, true><<<work_ctas, 256, 0, v->stream>>>(
                     p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
@@ -1209,7 +1104,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                     p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
                     v->d_work_n, v->work_cap);
             v->launches++;
-        } else if (plane) {
+        } else if (fan_plane) {
             const int cpr = (w + kChunk - 1) / kChunk;
             if (!v->d_work) {
                 v->work_cap = 1u << 20;
@@ -1218,76 +1113,21 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             }
             CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
             const int ntx = (cpr + kPlaneTW - 1) / kPlaneTW, nty = (h + kPlaneTH - 1) / kPlaneTH;
-            dim3 grid(ntx, m, nty), grid6((cpr + 5) / 6, m, nty);
-            const int tw = v->plane_tw_cur;
-            // the deferred-chunk pass is grid-strided over a worklist of a few entries per frame:
-            // a single frame must not pay for launching thousands of idle CTAs
-            const int work_ctas = std::min(4096, std::max(16, 8 * m));
-            const GridDev gd = dev_grid(v->d);
-#define LP(a, b, c)                                                                               \
-    if (tw == 6)                                                                                  \
-        k_pnn_plane<a, b, c, 6><<<grid6, 192, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0,\
-                                                          cal, v->d_fan, gd, v->acc, bx, stats,     \
-                                                          v->d_work, v->d_work_n, v->work_cap,      \
-                                                          1u << 20, v->plane_prefetch);             \
-    else                                                                                          \
-    k_pnn_plane<a, b, c, 4><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0,   \
-                                                      cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,  \
-                                                      v->d_work_n, v->work_cap, 1u << 20,          \
-                                                      v->plane_prefetch);                          \
-    k_pnn_work<a, b><<<work_ctas, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,\
-                                                     gd, v->acc, bx, stats, v->d_work, v->d_work_n, \
+            dim3 grid(ntx, m, nty);
+#define LP(a, b)                                                                                   \
+    k_pnn_plane<a, b, 1, 4><<<grid, 128, 0, v->stream>>>(p, pitch, fstride, w, h, cpr, fps + k0, cal,  \
+                                                      v->d_fan, gd, v->acc, bx, stats, v->d_work,     \
+                                                      v->d_work_n, v->work_cap, 1u << 20, 2);        \
+    k_pnn_work<a, b><<<work_ctas, 256, 0, v->stream>>>(p, pitch, fstride, w, fps + k0, cal, v->d_fan,  \
+                                                     gd, v->acc, bx, stats, v->d_work, v->d_work_n,   \
                                                      v->work_cap)
-            // k_pnn_lin's flush keeps byte offsets from the tile base in 32 bits: up to ~66
-            // planes of nx * ny voxels
-            if (v->plane_lin && v->plane_walk && vec && tw == 4 && w % (4 * kChunk) == 0 &&
-                cal.probe != SVR_PROBE_FAN && (long long)v->d.nx * v->d.ny * 8 * 72 < (1ll << 31)) {
-                // SVR_PLANE_LIN: 1 = 64 x 128 px tiles (4 chunks per thread), 2 = 64 x 64, 3 = 64 x 256
-                // a launch of a few frames (the per-frame path) takes 64-row tiles: twice the CTAs,
-                // half the pixels on each one's critical path
-                const int nch = (v->plane_lin == 2 || (v->plane_lin == 1 && m <= v->lin_small)) ? 2
-                                : v->plane_lin == 3 ? 8 : 4;
-                dim3 gl(ntx, m, (h + 32 * nch - 1) / (32 * nch));
-#define LL(bx_, n_)                                                                                 \
-    k_pnn_lin<bx_, n_, 4><<<gl, 128, 0, v->stream>>>(p, pitch, fstride, h, fps + k0, v->d_fan, gd, v->acc, \
-                                                     bx, stats, v->d_work, v->d_work_n, v->work_cap,  \
-                                                     1u << 20, v->plane_flush_lin)
-                if (box) { if (nch == 4) LL(true, 4); else if (nch == 8) LL(true, 8); else LL(true, 2); }
-                else { if (nch == 4) LL(false, 4); else if (nch == 8) LL(false, 8); else LL(false, 2); }
-#undef LL
-                if (box)
-                    k_pnn_work<true, true><<<work_ctas, 256, 0, v->stream>>>(
-                        p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
-                        v->d_work_n, v->work_cap);
-                else
-                    k_pnn_work<true, false><<<work_ctas, 256, 0, v->stream>>>(
-                        p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
-                        v->d_work_n, v->work_cap);
-            } else if (v->plane_walk) {
-                if (vec) {
-                    if (box) { LP(true, true, 1); } else { LP(true, false, 1); }
-                } else {
-                    if (box) { LP(false, true, 1); } else { LP(false, false, 1); }
-                }
+            if (vec) {
+                if (box) { LP(true, true); } else { LP(true, false); }
             } else {
-                if (vec) {
-                    if (box) { LP(true, true, 0); } else { LP(true, false, 0); }
-                } else {
-                    if (box) { LP(false, true, 0); } else { LP(false, false, 0); }
-                }
+                if (box) { LP(false, true); } else { LP(false, false); }
             }
 #undef LP
             v->launches += 2;
-        } else if (rows) {
-            if (vec) {
-                if (box) launch_rows_t<true, true>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
-                else launch_rows_t<true, false>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
-            } else {
-                if (box) launch_rows_t<false, true>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
-                else launch_rows_t<false, false>(v, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats);
-            }
-        } else if (tile) {
-            launch_tile(v, vec, skip, box, p, pitch, fstride, w, h, m, fps + k0, cal, ts, bx, stats);
         } else if (mode == kModeInsert) {
             launch_insert<kModeInsert>(v, vec, skip, box, p, pitch, fstride, w, h, m, fps + k0, cal,
                                        mark, tag, bx, stats);
@@ -1345,17 +1185,6 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
     // voxel table (x extent over 96 columns + 64 rows, plus the +-1 margins), else 4
     v->lin_shapes_cur = 0xf;
     for (int k = 0; k < n; ++k) v->lin_shapes_cur &= hp[k].lin_fit;
-    v->plane_tw_cur = 4;
-    if (v->plane_tw == 6 && c->probe != SVR_PROBE_FAN) {
-        double mx = 0.0, my = 0.0;
-        for (int k = 0; k < n; ++k) {
-            mx = std::max(mx, std::fabs((double)hp[k].Dc[0]) * 95.0 + std::fabs((double)hp[k].Dr[0]) * 63.0);
-            my = std::max(my, std::fabs((double)hp[k].Dc[1]) * 95.0 + std::fabs((double)hp[k].Dr[1]) * 63.0);
-        }
-        mx /= 4294967296.0;
-        my /= 4294967296.0;
-        if (std::ceil(mx) + 4 <= 32 && std::ceil(my) + 4 <= 32) v->plane_tw_cur = 6;
-    }
     CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
                        v->stream));
     CK(cudaEventRecord(v->params_ev[v->pslot], v->stream));
@@ -1522,68 +1351,12 @@ static dim3 grid_1d(long long n) {
     return dim3((unsigned)gx, (unsigned)((n + gx - 1) / gx));
 }
 
-// Launch the fill over a list of clipped, non-empty boxes.
-// Tensor map of the accumulator slab for k_fill_tma: u64 elements, dims (nx, ny, nzl), box
-// (130, 18, 1), zero fill out of bounds.  Needs 16-byte row strides (nx even).
-static bool fill_tmap(svr_volume* v) {
-    if (v->tmap_state) return v->tmap_state > 0;
-    v->tmap_state = -1;
-    if (v->d.nx % 2) return false;
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
-        q != cudaDriverEntryPointSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    const cuuint64_t dims[3] = {(cuuint64_t)v->d.nx, (cuuint64_t)v->d.ny, (cuuint64_t)(v->d.z_end - v->d.z_begin)};
-    const cuuint64_t strides[2] = {(cuuint64_t)v->d.nx * 8, (cuuint64_t)v->d.nx * v->d.ny * 8};
-    const cuuint32_t box[3] = {kFtBX, kFtBY, 1}, es[3] = {1, 1, 1};
-    CUresult r = ((Encode)fn)(&v->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, v->acc, dims, strides, box, es,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return false;
-    const int smem = (int)kFtSmemBytes;
-    if (cudaFuncSetAttribute(k_fill_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_fill_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    v->tmap_state = 1;
-    return true;
-}
-
+// Launch the fill over a list of clipped, non-empty boxes: the BASELINE mean r = 1 by
+// k_fill_warp (one launch over all boxes), everything else (SPEC median, mean r = 2) by
+// k_fill_generic per box.
 static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, int32_t radius, bool count) {
     const GridDev g = dev_grid(v->d);
-    if (mode == SVR_FILL_MEAN && radius == 1 && v->fill_tma && !v->fill_smem && fill_tmap(v)) {
-        const int zc = v->fill_tma_zc;
-        std::vector<BoxTiles> bt;
-        long long total = 0;
-        for (const Box& b : bs) {
-            BoxTiles t;
-            t.b = b;
-            t.ntx = (b.x1 - b.x0 + 1 + kFtX - 1) / kFtX;
-            t.nty = (b.y1 - b.y0 + 1 + kFtY - 1) / kFtY;
-            t.first = total;
-            total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
-            bt.push_back(t);
-        }
-        void* d = nullptr;
-        if (int e = upload_tiles(v, bt.data(), sizeof(BoxTiles) * bt.size(), &d)) return e;
-        const dim3 grd = grid_1d(total);
-        const size_t smem = kFtSmemBytes;
-        if (zc == 16)
-            k_fill_tma<16><<<grd, 128, smem, v->stream>>>(v->tmap, v->fill, g, (const BoxTiles*)d, (int)bt.size(), v->d_counter);
-        else
-            k_fill_tma<32><<<grd, 128, smem, v->stream>>>(v->tmap, v->fill, g, (const BoxTiles*)d, (int)bt.size(), v->d_counter);
-        v->launches++;
-        CKL();
-        return SVR_OK;
-    }
-    if (mode == SVR_FILL_MEAN && radius == 1 && !v->fill_smem) {
+    if (mode == SVR_FILL_MEAN && radius == 1) {
         std::vector<BoxTiles> bt;
         long long total = 0;
         auto tile = [&](int zc) {
@@ -1592,19 +1365,19 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
             for (const Box& b : bs) {
                 BoxTiles t;
                 t.b = b;
-                t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of fill_ty rows
-                t.nty = (b.y1 - b.y0 + 1 + 4 * v->fill_ty - 1) / (4 * v->fill_ty);
+                t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of 8 rows
+                t.nty = (b.y1 - b.y0 + 1 + 31) / 32;
                 t.first = total;
                 total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
                 bt.push_back(t);
             }
         };
-        // planes per march: SVR_FILL_ZC, else 32 unless that leaves fewer than ~8 CTAs per SM
-        // (a slab's share of a multi-GPU split, small incremental boxes): then 16 or 8
-        int zc = v->fill_zc > 0 ? v->fill_zc : 32;
+        // planes per march: 32, unless that leaves fewer than ~8 CTAs per SM (a slab's share of a
+        // multi-GPU split, small incremental boxes): then 16 or 8
+        int zc = 32;
         tile(zc);
         const long long want = 8ll * v->num_sms;
-        while (v->fill_zc <= 0 && v->fill_depth != 2 && v->fill_ty == 8 && zc > 8 && total < want) {
+        while (zc > 8 && total < want) {
             zc /= 2;
             tile(zc);
         }
@@ -1613,26 +1386,15 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         const dim3 grd = grid_1d(total);
         const BoxTiles* dt = (const BoxTiles*)d;
         const int nb = (int)bt.size();
-#define FW(Z, D, T) k_fill_warp<Z, D, T><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, v->d_counter)
-        const int ty = v->fill_ty;
-        if (v->fill_depth == 2) {
-            if (zc == 8) FW(8, 2, 8);
-            else if (zc == 32) FW(32, 2, 8);
-            else FW(16, 2, 8);
-        } else if (ty == 4) {
-            FW(16, 1, 4);
-        } else if (ty == 12) {
-            FW(16, 1, 12);
-        } else if (ty == 16) {
-            FW(16, 1, 16);
+#define FW(Z, C) k_fill_warp<Z, 1, 8, C><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, C ? v->d_counter : nullptr)
+        if (count) {
+            if (zc == 8) FW(8, true);
+            else if (zc == 16) FW(16, true);
+            else FW(32, true);
         } else {
-            if (!count) {
-                if (zc == 8) k_fill_warp<8, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
-                else if (zc == 32) k_fill_warp<32, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
-                else k_fill_warp<16, 1, 8, false><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, nullptr);
-            } else if (zc == 8) FW(8, 1, 8);
-            else if (zc == 32) FW(32, 1, 8);
-            else FW(16, 1, 8);
+            if (zc == 8) FW(8, false);
+            else if (zc == 16) FW(16, false);
+            else FW(32, false);
         }
 #undef FW
         v->launches++;
@@ -1640,23 +1402,8 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         return SVR_OK;
     }
     for (const Box& b : bs) {
-        const int bx = b.x1 - b.x0 + 1, by = b.y1 - b.y0 + 1, bz = b.z1 - b.z0 + 1;
-        if (mode == SVR_FILL_MEAN && radius <= 2) {
-            dim3 grd((bx + 31) / 32, (by + 7) / 8, (bz + 31) / 32);
-            if (radius == 1)
-                k_fill_sep<1><<<grd, dim3(34, 10), 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
-            else
-                k_fill_sep<2><<<grd, dim3(36, 12), 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
-        } else if (radius == 1) {
-            dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 15) / 16);
-            k_fill<1, SVR_FILL_MEDIAN, 32, 8, 16><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
-        } else if (radius == 2) {
-            dim3 blk(32, 8), grd((bx + 31) / 32, (by + 7) / 8, (bz + 7) / 8);
-            k_fill<2, SVR_FILL_MEDIAN, 32, 8, 8><<<grd, blk, 0, v->stream>>>(v->acc, v->fill, g, b, v->d_counter);
-        } else {
-            long long nv = (long long)bx * by * bz;
-            k_fill_generic<<<(unsigned)((nv + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, g, b, radius, mode, v->d_counter);
-        }
+        const long long nv = (long long)(b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1) * (b.z1 - b.z0 + 1);
+        k_fill_generic<<<(unsigned)((nv + 255) / 256), 256, 0, v->stream>>>(v->acc, v->fill, g, b, radius, mode, v->d_counter);
         v->launches++;
         CKL();
     }
@@ -1781,7 +1528,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
         }
     }
     if (dt.empty()) return SVR_OK;
-    const long long nd = tile_cols(dt, 128 / v->depth_seg), nm = tile_cols(mt);
+    const long long nd = tile_cols(dt, 128 / 4), nm = tile_cols(mt);  // k_depth<4>: 4 threads per column
     // one upload holds both tables: [dt | mt]
     std::vector<ColTiles> both(dt);
     both.insert(both.end(), mt.begin(), mt.end());
@@ -1803,15 +1550,8 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
         CKL();
         return SVR_OK;
     }
-    if (v->depth_seg == 8)
-        k_depth<8><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
-                                                        p->fill_mode, v->r_depth);
-    else if (v->depth_seg == 4)
-        k_depth<4><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
-                                                        p->fill_mode, v->r_depth);
-    else
-        k_depth<1><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
-                                                        p->fill_mode, v->r_depth);
+    k_depth<4><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
+                                                    p->fill_mode, v->r_depth);
     v->launches++;
     CKL();
     k_band<false><<<grid_1d(nm), 128, 0, v->stream>>>(v->acc, v->fill, g, dmt, (int)mt.size(), p->median_radius,
@@ -2247,7 +1987,7 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm) || !shape_ok) {
         v->lin_shapes_cur = fpar.lin_fit;
         if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;
-        f.shape = pick_shape(fpar.lin_fit, w, 1, v->lin_small);
+        f.shape = pick_shape(fpar.lin_fit, w, 1, kLinSmall);
         ++f.captures;
     }
     *f.h_fp = fpar;

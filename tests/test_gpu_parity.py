@@ -38,9 +38,7 @@ def test_cfg1_batch_bitexact():
     assert st["frames_inserted"] == wl.nframes
 
 
-@pytest.mark.parametrize("depth_seg", ["4", "1"])
-def test_cfg1_fill_and_render_bitexact(depth_seg, monkeypatch):
-    monkeypatch.setenv("SVR_DEPTH_SEG", depth_seg)  # k_depth: 4 threads per column, or 1
+def test_cfg1_fill_and_render_bitexact():
     wl = synth.cfg1()
     frames = wl.frames_np()
     grid = _grid(wl)
@@ -303,15 +301,16 @@ def test_footprint_counts():
         assert u[k] == int((r.count > 0).sum())
 
 
-INSERT_KERNELS = ["plane", "plane-carry", "plane-tw6", "direct", "rows", "tile"]
+INSERT_KERNELS = ["auto", "direct"]
 
 
 def _select_kernel(monkeypatch, kernel):
-    """SVR_INSERT_KERNEL (+ SVR_PLANE_WALK=0 for the carry-walk form of k_pnn_plane,
-    SVR_PLANE_TW=6 for its 96-px tiles)."""
-    monkeypatch.setenv("SVR_INSERT_KERNEL", kernel.split("-")[0])
-    monkeypatch.setenv("SVR_PLANE_WALK", "0" if kernel == "plane-carry" else "1")
-    monkeypatch.setenv("SVR_PLANE_TW", "6" if kernel == "plane-tw6" else "4")
+    """auto: the launch's own choice (k_pnn_tiles for linear probes whose tiles fit, k_pnn_plane
+    for fans, k_insert otherwise); direct: SVR_INSERT_KERNEL=direct forces the k_insert fallback."""
+    if kernel == "direct":
+        monkeypatch.setenv("SVR_INSERT_KERNEL", "direct")
+    else:
+        monkeypatch.delenv("SVR_INSERT_KERNEL", raising=False)
 
 
 @pytest.mark.parametrize("name", ["small_linear", "small_fan"])
@@ -355,11 +354,10 @@ def test_cfg1_all_kernels(kernel, monkeypatch):
     assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
 
 
-@pytest.mark.parametrize("fill_kernel", ["tma", "warp", "smem"])
-def test_mean_fill_kernels_bitexact(fill_kernel, monkeypatch):
-    """Both r=1 mean-fill kernels (register/shuffle and shared-memory separable) against the
-    oracle on a region with grid-edge clipping."""
-    monkeypatch.setenv("SVR_FILL_KERNEL", fill_kernel)
+@pytest.mark.parametrize("radius", [1, 2])
+def test_mean_fill_bitexact(radius):
+    """Mean fill (r = 1: k_fill_warp; r = 2: k_fill_generic) against the oracle on regions with
+    grid-edge clipping."""
     wl = synth.cfg1(nframes=80)
     frames = wl.frames_np()
     grid = _grid(wl)
@@ -367,18 +365,16 @@ def test_mean_fill_kernels_bitexact(fill_kernel, monkeypatch):
     ref = O.OracleGrid.for_workload(wl)
     ref.insert_frames(frames, wl.poses, wl.calib)
     for region in (None, (3, 0, 20, 200, 127, 70), (0, 5, 0, 127, 60, 255)):
-        n = grid.fill_holes(region, 1, pkg.FILL_MEAN)
-        nr = ref.fill_holes(region, 0, 1)
+        n = grid.fill_holes(region, radius, pkg.FILL_MEAN)
+        nr = ref.fill_holes(region, 0, radius)
         assert n == nr, region
         assert np.array_equal(grid.fill_layer(), ref.fill), region
 
 
-@pytest.mark.parametrize("fill_kernel", ["tma", "warp", "smem"])
-def test_fill_large_accumulators(fill_kernel, monkeypatch):
+def test_fill_large_accumulators():
     """Voxel values from counts up to the u16 maximum and sums past 2^23 (outside the fp32
     estimate's exact range: the fill kernels' recompute path) feed the neighbours' mean fills
     exactly as in the oracle."""
-    monkeypatch.setenv("SVR_FILL_KERNEL", fill_kernel)
     dims = (70, 40, 50)
     rng = np.random.default_rng(21)
     shp = (dims[2], dims[1], dims[0])
@@ -427,13 +423,11 @@ def test_chunked_dirty_regions_equal_bounding_box():
 
 
 def test_cfg2_full_size_properties(monkeypatch):
-    """BASELINE cfg2 at full size (2400 x 512 x 480 frames, 500 x 267 x 2000 grid), through
-    size-independent properties: every pixel lands (no OOB) and the accumulators conserve the
-    pixel count and the pixel sum exactly; a reversed frame order through the direct kernel gives
-    identical accumulators (order independence); the fill over the per-chunk dirty
-    boxes and its count agree between the register, TMA and shared-memory fill kernels."""
+    """BASELINE cfg2 at full size through size-independent properties (the bit-exact oracle
+    comparison is tests/test_gpu_fullsize.py): every pixel lands (no OOB) and the accumulators
+    conserve the pixel count and sum exactly; the reversed frame order through the direct fallback
+    kernel gives identical accumulators (order independence)."""
     import torch
-    from paper_2412_00058_b200 import sharding
     wl = synth.cfg2()
     frames = torch.empty((wl.nframes, wl.h, wl.w), dtype=torch.uint8, device="cuda")
     synth.synth_frames_device(wl, frames, 0, wl.nframes)
@@ -452,21 +446,6 @@ def test_cfg2_full_size_properties(monkeypatch):
     b.insert_frames(rev, wl.poses[::-1].copy(), wl.calib)
     s2, c2 = b.accumulators()
     assert np.array_equal(c, c2) and np.array_equal(s, s2)
-    del s2, c2, rev, b
-    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
-    fb = sharding.chunk_boxes(boxes, np.arange(len(boxes)), (0, wl.dims[2]), chunk=32, dilate=1)
-    ref_fill, ref_n = None, None
-    for kernel in ("warp", "tma", "smem"):
-        monkeypatch.setenv("SVR_FILL_KERNEL", kernel)
-        g = _grid(wl)
-        g.insert_frames(frames, wl.poses, wl.calib)
-        n = g.fill_holes_boxes(fb, 1, pkg.FILL_MEAN)
-        fl = g.fill_layer()
-        if ref_fill is None:
-            ref_fill, ref_n = fl, n
-        else:
-            assert n == ref_n and np.array_equal(fl, ref_fill), kernel
-        del g
 
 
 @pytest.mark.parametrize("world", [2, 3])
