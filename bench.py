@@ -101,31 +101,79 @@ def sample_frames(wl, every):
     return idx, frames
 
 
+def _cfg2_frames_host(wl):
+    """All cfg2 frames in host memory (the device generator when a GPU is present, else numpy;
+    data preparation, outside every timed region)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            from paper_2412_00058_b200 import synth
+            dev = torch.empty((wl.nframes, wl.h, wl.w), dtype=torch.uint8, device="cuda")
+            synth.synth_frames_device(wl, dev, 0, wl.nframes)
+            out = dev.cpu().numpy()
+            del dev
+            torch.cuda.empty_cache()
+            return out
+    except Exception:
+        pass
+    return wl.frames_np()
+
+
 def run_reference(args):
+    """The reference's CPU path on the bench's own step: all 2400 cfg2 frames inserted by the
+    reference's spinevol::pixel_to_world + SPEC insert loop (oracle/_ref, z-slab threads), then
+    the 3x3x3 mean fill of the same per-z-chunk dirty boxes and the cfg4 depth-band render of the
+    same columns by the C restatement (the reference has no fill / render code), all host threads."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2412_00058_b200 import synth
+    from oracle import oracle as O
+    from paper_2412_00058_b200 import sharding, synth
     wl = synth.cfg2()
-    every = args.ref_every
-    idx, frames = sample_frames(wl, every)
+    frames = _cfg2_frames_host(wl)
     nth = _ncpu()
-    kind, _, px = cpu_reference(wl, frames[:4], wl.poses[idx[:4]], nth)  # load + page in
-    step_times = []
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    idx = np.arange(wl.nframes)
+    fb = sharding.chunk_boxes(boxes, idx, (0, wl.dims[2]), chunk=32, dilate=wl.fill_radius)
+    rb = sharding.chunk_boxes(boxes, idx, (0, wl.dims[2]), chunk=32)
+    rp = synth.render_params()
+    grid = O.OracleGrid.for_workload(wl)
+    kind = "reference" if O.ref() is not None else "port"
+
+    def step():
+        t = [time.perf_counter()]
+        if kind == "reference":
+            O.ref_insert_frames(wl.dims, wl.voxel_mm, wl.origin, frames, wl.poses, wl.calib,
+                                nthreads=nth, out=(grid.sum, grid.count))
+        else:
+            grid.insert_frames_mt(frames, wl.poses, wl.calib, nthreads=nth)
+        t.append(time.perf_counter())
+        grid.fill_holes_boxes_mt(fb, 0, wl.fill_radius, nthreads=nth)
+        t.append(time.perf_counter())
+        grid.render_boxes_mt(rp, rb, wl.fill_radius, nthreads=nth)
+        t.append(time.perf_counter())
+        return t[3] - t[0], (t[1] - t[0], t[2] - t[1], t[3] - t[2])
+
+    step_times, stages = [], []
     for i in range(args.warmup + args.steps):
-        _, t, px = cpu_reference(wl, frames, wl.poses[idx], nth)
+        tt, st = step()
         if i >= args.warmup:
-            step_times.append(t[0])
+            step_times.append(tt)
+            stages.append(st)
     tot = sum(step_times)
+    px = wl.nframes * wl.w * wl.h
     value = px * len(step_times) / tot / 1e9
-    sample = ("%d of 2400 cfg2 frames (every %dth, %.1f Mpx) per step; PNN insert only (the "
-              "reference's spinevol::pixel_to_world + SPEC insert loop), %d threads, %s"
-              % (len(idx), every, px / 1e6, nth, _cpu_model()))
+    sample = ("the whole bench step: all 2400 cfg2 frames (%.0f Mpx) inserted by the reference's "
+              "spinevol::pixel_to_world + SPEC insert loop (%s), mean fill r=1 of the %d per-z-chunk "
+              "dirty boxes and the cfg4 render of the %d column boxes by the C restatement; %d threads, %s"
+              % (px / 1e6, kind, len(fb), len(rb), nth, _cpu_model()))
+    stage_ms = {k: 1e3 * sum(st[i] for st in stages) / len(stages) for i, k in enumerate(("insert", "fill", "render"))}
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(step_times) * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
            "data": "synthetic (seeded, BASELINE cfg2 generator)",
-           "config": {"workload": WORKLOAD, "sample": sample},
+           "config": {"workload": WORKLOAD, "sample": sample, "same_config": True},
+           "stages_ms": stage_ms,
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": kind, "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

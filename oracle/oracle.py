@@ -58,6 +58,10 @@ def lib():
         L.orc_fill_holes.restype = C.c_int64
         L.orc_values.argtypes = [PG, C.c_int32, P]
         L.orc_render.argtypes = [PG, PB, C.c_int32, C.POINTER(RenderParams), P, P, P, P]
+        L.orc_fill_holes_boxes_mt.argtypes = [PG, PB, C.c_int32, C.c_int32, C.c_int32, C.c_int32]
+        L.orc_fill_holes_boxes_mt.restype = C.c_int64
+        L.orc_render_boxes_mt.argtypes = [PG, PB, C.c_int32, C.c_int32, C.POINTER(RenderParams), P, P, P,
+                                          P, C.c_int32]
         L.orc_render_ints.argtypes = [C.POINTER(RenderParams), C.c_double, C.c_int32] + [C.POINTER(C.c_int32)] * 4
         L.orc_coronal_projection.argtypes = [PG, C.c_int32, C.c_int32, C.c_int32, P]
         L.orc_cut_depth_alg1.argtypes = [C.c_double] * 6
@@ -197,6 +201,18 @@ class OracleGrid:
     def fill_holes(self, region=None, mode=0, radius=1) -> int:
         b = None if region is None else C.byref(region if isinstance(region, Box) else Box(*region))
         return int(lib().orc_fill_holes(C.byref(self.g), b, mode, radius))
+
+    def fill_holes_boxes_mt(self, boxes, mode=0, radius=1, nthreads=None) -> int:
+        arr = (Box * max(len(boxes), 1))(*[b if isinstance(b, Box) else Box(*b) for b in boxes])
+        return int(lib().orc_fill_holes_boxes_mt(C.byref(self.g), arr, len(boxes), mode, radius,
+                                                 nthreads or os.cpu_count() or 1))
+
+    def render_boxes_mt(self, params, boxes, fill_radius=1, nthreads=None):
+        arr = (Box * max(len(boxes), 1))(*[b if isinstance(b, Box) else Box(*b) for b in boxes])
+        lib().orc_render_boxes_mt(C.byref(self.g), arr, len(boxes), fill_radius, C.byref(params),
+                                  self.mean.ctypes.data, self.max.ctypes.data, self.depth.ctypes.data,
+                                  self.mdepth.ctypes.data, nthreads or os.cpu_count() or 1)
+        return self.mean, self.max, self.mdepth
 
     def values(self, apply_fills=False):
         out = np.empty_like(self.sum, dtype=np.uint8)

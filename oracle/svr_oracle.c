@@ -478,51 +478,55 @@ static int cmp_i32(const void* a, const void* b) {
 
 /* Depth-band coronal render (BASELINE cfg4), images are (z_end-z_begin) x nx, x fastest.
  * Incremental: depths recomputed on dirty (+) fill_radius (x,z), median+band on that (+) R. */
-void orc_render(const orc_grid* g, const svr_box* dirty, int32_t fill_radius,
-                const svr_render_params* p, float* mean, float* maxv, int32_t* depth,
-                int32_t* mdepth) {
+/* the rows [z0, z1] of one render region (orc_render's dilations and clipping) */
+static void render_ranges(const orc_grid* g, const svr_box* dirty, int32_t fr, int32_t R, int32_t* d,
+                          int32_t* m) {
+    int32_t dx0 = dirty->x0 - fr, dx1 = dirty->x1 + fr, dz0 = dirty->z0 - fr, dz1 = dirty->z1 + fr;
+    int32_t mx0 = dx0 - R, mx1 = dx1 + R, mz0 = dz0 - R, mz1 = dz1 + R;
+#define CLX(a) ((a) < 0 ? 0 : ((a) > g->nx - 1 ? g->nx - 1 : (a)))
+#define CLZ(a) ((a) < g->z_begin ? g->z_begin : ((a) > g->z_end - 1 ? g->z_end - 1 : (a)))
+    d[0] = CLX(dx0); d[1] = CLX(dx1); d[2] = CLZ(dz0); d[3] = CLZ(dz1);
+    m[0] = CLX(mx0); m[1] = CLX(mx1); m[2] = CLZ(mz0); m[3] = CLZ(mz1);
+#undef CLX
+#undef CLZ
+}
+
+/* One pass of the render over the (already dilated and clipped) column range of `r`:
+ * pass 1 computes column depths over x in [r.x0, r.x1], z in [r.z0, r.z1]; pass 2 the median
+ * and band of the same range.  orc_render runs pass 1 over the dirty region (+ fill radius) and
+ * pass 2 over that (+ median radius). */
+void orc_render_pass(const orc_grid* g, const svr_box* r, int32_t pass, const svr_render_params* p,
+                     float* mean, float* maxv, int32_t* depth, int32_t* mdepth) {
     int32_t ylo, yhi, above, below;
     orc_render_ints(p, g->voxel_mm, g->ny, &ylo, &yhi, &above, &below);
     const int32_t R = p->median_radius;
-    int32_t dx0 = 0, dx1 = g->nx - 1, dz0 = g->z_begin, dz1 = g->z_end - 1;
-    if (dirty) {
-        if (dirty->x0 > dirty->x1) return;
-        dx0 = dirty->x0 - fill_radius;
-        dx1 = dirty->x1 + fill_radius;
-        dz0 = dirty->z0 - fill_radius;
-        dz1 = dirty->z1 + fill_radius;
-    }
-    int32_t mx0 = dx0 - R, mx1 = dx1 + R, mz0 = dz0 - R, mz1 = dz1 + R;
-#define CLIPX(a) ((a) < 0 ? 0 : ((a) > g->nx - 1 ? g->nx - 1 : (a)))
-#define CLIPZ(a) ((a) < g->z_begin ? g->z_begin : ((a) > g->z_end - 1 ? g->z_end - 1 : (a)))
-    dx0 = CLIPX(dx0); dx1 = CLIPX(dx1); mx0 = CLIPX(mx0); mx1 = CLIPX(mx1);
-    dz0 = CLIPZ(dz0); dz1 = CLIPZ(dz1); mz0 = CLIPZ(mz0); mz1 = CLIPZ(mz1);
     const int64_t sz = (int64_t)g->nx * g->ny;
-    /* pass 1: column depth = first argmax of the forward gradient */
-    for (int32_t z = dz0; z <= dz1; ++z)
-        for (int32_t x = dx0; x <= dx1; ++x) {
-            int64_t base = (int64_t)(z - g->z_begin) * sz + x;
-            int valid = 0;
-            float prev = 0.0f;
-            if (ylo <= yhi) {
-                float fv;
-                if (voxel_f(g, base + (int64_t)ylo * g->nx, p->fill_mode, &fv)) { prev = fv; valid = 1; }
+    if (pass == 1) {
+        for (int32_t z = r->z0; z <= r->z1; ++z)
+            for (int32_t x = r->x0; x <= r->x1; ++x) {
+                int64_t base = (int64_t)(z - g->z_begin) * sz + x;
+                int valid = 0;
+                float prev = 0.0f;
+                if (ylo <= yhi) {
+                    float fv;
+                    if (voxel_f(g, base + (int64_t)ylo * g->nx, p->fill_mode, &fv)) { prev = fv; valid = 1; }
+                }
+                float best = 0.0f;
+                int32_t arg = -1;
+                for (int32_t y = ylo; y <= yhi; ++y) {
+                    float nxt = 0.0f, fv;
+                    if (voxel_f(g, base + (int64_t)(y + 1) * g->nx, p->fill_mode, &fv)) { nxt = fv; valid = 1; }
+                    float gr = nxt - prev;
+                    if (arg < 0 || gr > best) { best = gr; arg = y; }
+                    prev = nxt;
+                }
+                depth[(int64_t)(z - g->z_begin) * g->nx + x] = valid ? arg : -1;
             }
-            float best = 0.0f;
-            int32_t arg = -1;
-            for (int32_t y = ylo; y <= yhi; ++y) {
-                float nxt = 0.0f, fv;
-                if (voxel_f(g, base + (int64_t)(y + 1) * g->nx, p->fill_mode, &fv)) { nxt = fv; valid = 1; }
-                float gr = nxt - prev;
-                if (arg < 0 || gr > best) { best = gr; arg = y; }
-                prev = nxt;
-            }
-            depth[(int64_t)(z - g->z_begin) * g->nx + x] = valid ? arg : -1;
-        }
-    /* pass 2: (2R+1)^2 lower median of valid depths, then mean/max over the band */
+        return;
+    }
     int32_t* win = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * R + 1) * (2 * R + 1));
-    for (int32_t z = mz0; z <= mz1; ++z)
-        for (int32_t x = mx0; x <= mx1; ++x) {
+    for (int32_t z = r->z0; z <= r->z1; ++z)
+        for (int32_t x = r->x0; x <= r->x1; ++x) {
             int n = 0;
             for (int32_t zz = z - R; zz <= z + R; ++zz) {
                 if (zz < g->z_begin || zz >= g->z_end) continue;
@@ -565,8 +569,23 @@ void orc_render(const orc_grid* g, const svr_box* dirty, int32_t fill_radius,
             maxv[o] = mx;
         }
     free(win);
-#undef CLIPX
-#undef CLIPZ
+}
+
+void orc_render(const orc_grid* g, const svr_box* dirty, int32_t fill_radius,
+                const svr_render_params* p, float* mean, float* maxv, int32_t* depth,
+                int32_t* mdepth) {
+    svr_box all = {0, 0, g->z_begin, g->nx - 1, g->ny - 1, g->z_end - 1};
+    if (dirty && dirty->x0 > dirty->x1) return;
+    int32_t d[4], m[4];
+    if (dirty) {
+        render_ranges(g, dirty, fill_radius, p->median_radius, d, m);
+    } else {
+        d[0] = m[0] = 0; d[1] = m[1] = g->nx - 1; d[2] = m[2] = g->z_begin; d[3] = m[3] = g->z_end - 1;
+    }
+    (void)all;
+    svr_box r1 = {d[0], 0, d[2], d[1], g->ny - 1, d[3]}, r2 = {m[0], 0, m[2], m[1], g->ny - 1, m[3]};
+    orc_render_pass(g, &r1, 1, p, mean, maxv, depth, mdepth);
+    orc_render_pass(g, &r2, 2, p, mean, maxv, depth, mdepth);
 }
 
 /* coronal_projection: max, or mean over non-empty voxels (round like
@@ -795,4 +814,114 @@ int orc_smooth_depths(const double* d, const uint8_t* valid, int32_t n, int32_t 
     free(win);
     free(g);
     return 0;
+}
+
+
+/* ---- multi-threaded fill + render over box lists (CPU baseline of the whole bench step) ----
+ * Threads split each box's z range; the fill writes only its own voxels and reads only the
+ * accumulators, the render's first pass (column depths) completes for every box before the
+ * second (median + band) reads them -- the same results as the single-threaded functions. */
+typedef struct {
+    orc_grid* g;
+    const svr_box* boxes;
+    int32_t n, mode, radius, tid, nthreads;
+    int64_t filled;
+} fill_job;
+
+static void* fill_worker(void* arg) {
+    fill_job* j = (fill_job*)arg;
+    for (int32_t i = 0; i < j->n; ++i) {
+        svr_box b = j->boxes[i];
+        if (b.z0 < j->g->z_begin) b.z0 = j->g->z_begin;
+        if (b.z1 > j->g->z_end - 1) b.z1 = j->g->z_end - 1;
+        const int32_t len = b.z1 - b.z0 + 1;
+        if (len <= 0) continue;
+        svr_box sub = b;
+        sub.z0 = b.z0 + (int32_t)((int64_t)len * j->tid / j->nthreads);
+        sub.z1 = b.z0 + (int32_t)((int64_t)len * (j->tid + 1) / j->nthreads) - 1;
+        if (sub.z0 > sub.z1) continue;
+        j->filled += orc_fill_holes(j->g, &sub, j->mode, j->radius);
+    }
+    return NULL;
+}
+
+int64_t orc_fill_holes_boxes_mt(orc_grid* g, const svr_box* boxes, int32_t n, int32_t mode,
+                                int32_t radius, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    fill_job* jobs = (fill_job*)calloc((size_t)nthreads, sizeof(fill_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        fill_job jb = {g, boxes, n, mode, radius, t, nthreads, 0};
+        jobs[t] = jb;
+        pthread_create(&th[t], NULL, fill_worker, &jobs[t]);
+    }
+    int64_t filled = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        pthread_join(th[t], NULL);
+        filled += jobs[t].filled;
+    }
+    g->fill_mode = mode;
+    free(jobs);
+    free(th);
+    return filled;
+}
+
+typedef struct {
+    const orc_grid* g;
+    const svr_box* boxes;
+    int32_t n, fill_radius, tid, nthreads;
+    const svr_render_params* p;
+    float *mean, *maxv;
+    int32_t *depth, *mdepth;
+    pthread_barrier_t* bar;
+} render_job;
+
+static void* render_worker(void* arg) {
+    render_job* j = (render_job*)arg;
+    const orc_grid* g = j->g;
+    const svr_render_params* p = j->p;
+    int32_t ylo, yhi, above, below;
+    orc_render_ints(p, g->voxel_mm, g->ny, &ylo, &yhi, &above, &below);
+    const int32_t R = p->median_radius;
+    for (int pass = 1; pass <= 2; ++pass) {
+        for (int32_t i = 0; i < j->n; ++i) {
+            if (j->boxes[i].x0 > j->boxes[i].x1) continue;
+            int32_t d[4], m[4];
+            render_ranges(g, &j->boxes[i], j->fill_radius, R, d, m);
+            const int32_t* r = pass == 1 ? d : m;
+            const int32_t len = r[3] - r[2] + 1;
+            if (len <= 0) continue;
+            /* this thread's rows, as a region whose dilation reproduces exactly them */
+            svr_box sub;
+            sub.x0 = r[0];
+            sub.x1 = r[1];
+            sub.z0 = r[2] + (int32_t)((int64_t)len * j->tid / j->nthreads);
+            sub.z1 = r[2] + (int32_t)((int64_t)len * (j->tid + 1) / j->nthreads) - 1;
+            if (sub.z0 > sub.z1) continue;
+            sub.y0 = 0;
+            sub.y1 = g->ny - 1;
+            orc_render_pass(g, &sub, pass, p, j->mean, j->maxv, j->depth, j->mdepth);
+        }
+        pthread_barrier_wait(j->bar);
+    }
+    return NULL;
+}
+
+void orc_render_boxes_mt(const orc_grid* g, const svr_box* boxes, int32_t n, int32_t fill_radius,
+                         const svr_render_params* p, float* mean, float* maxv, int32_t* depth,
+                         int32_t* mdepth, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)nthreads);
+    render_job* jobs = (render_job*)calloc((size_t)nthreads, sizeof(render_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        render_job jb = {g, boxes, n, fill_radius, t, nthreads, p, mean, maxv, depth, mdepth, &bar};
+        jobs[t] = jb;
+        pthread_create(&th[t], NULL, render_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    pthread_barrier_destroy(&bar);
+    free(jobs);
+    free(th);
 }

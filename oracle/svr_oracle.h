@@ -69,6 +69,14 @@ void orc_render_ints(const svr_render_params* p, double voxel_mm, int32_t ny, in
 void orc_render(const orc_grid* g, const svr_box* dirty, int32_t fill_radius,
                 const svr_render_params* p, float* mean, float* maxv, int32_t* depth,
                 int32_t* mdepth);
+void orc_render_pass(const orc_grid* g, const svr_box* r, int32_t pass, const svr_render_params* p,
+                     float* mean, float* maxv, int32_t* depth, int32_t* mdepth);
+/* multithreaded fill / render over box lists (the CPU baseline of the bench step) */
+int64_t orc_fill_holes_boxes_mt(orc_grid* g, const svr_box* boxes, int32_t n, int32_t mode,
+                                int32_t radius, int32_t nthreads);
+void orc_render_boxes_mt(const orc_grid* g, const svr_box* boxes, int32_t n, int32_t fill_radius,
+                         const svr_render_params* p, float* mean, float* maxv, int32_t* depth,
+                         int32_t* mdepth, int32_t nthreads);
 void orc_coronal_projection(const orc_grid* g, int32_t mode, int32_t depth_axis,
                             int32_t use_fills, uint8_t* out);
 

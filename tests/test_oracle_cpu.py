@@ -325,3 +325,29 @@ def test_two_rank_gloo_slab_sharding_matches_unsharded():
         res = open(out).read()
     assert res.startswith("ok"), res
 
+
+
+def test_oracle_mt_fill_render_equal_single_thread():
+    """The multithreaded oracle fill / render over box lists (the CPU baseline of the bench step)
+    equal the single-threaded functions box by box."""
+    from paper_2412_00058_b200 import sharding
+    wl = synth.cfg1(nframes=60)
+    frames = wl.frames_np()
+    a = O.OracleGrid.for_workload(wl)
+    a.insert_frames_mt(frames, wl.poses, wl.calib)
+    b = O.OracleGrid.for_workload(wl)
+    b.sum[...] = a.sum
+    b.count[...] = a.count
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    idx = np.arange(len(boxes))
+    fb = sharding.chunk_boxes(boxes, idx, (0, wl.dims[2]), chunk=16, dilate=1)
+    rb = sharding.chunk_boxes(boxes, idx, (0, wl.dims[2]), chunk=16)
+    for bx in fb:
+        a.fill_holes(bx, 0, 1)
+    b.fill_holes_boxes_mt(fb, 0, 1, nthreads=5)
+    assert np.array_equal(a.fill, b.fill)
+    rp = synth.render_params()
+    a.render(rp, None, 1)  # single-threaded: every column
+    m1, x1, d1 = a.mean.copy(), a.max.copy(), a.mdepth.copy()
+    b.render_boxes_mt(rp, [pkg.Box(0, 0, 0, wl.dims[0] - 1, wl.dims[1] - 1, wl.dims[2] - 1)], 1, nthreads=7)
+    assert np.array_equal(b.mdepth, d1) and np.array_equal(b.mean, m1) and np.array_equal(b.max, x1)
