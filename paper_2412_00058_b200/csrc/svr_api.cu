@@ -1659,10 +1659,11 @@ extern "C" int svr_read_accumulators(svr_volume* v, const svr_box* box, uint32_t
     if (tc) CK(cudaFreeAsync(tc, v->stream));
     CK(cudaStreamSynchronize(v->stream));
     if (sat) {
-        // record in stats: voxels above the caps at readout
+        // record in stats: the most voxels above the caps any readout has seen
+        // (a readout of a sub-box must not erase a larger count from an earlier one)
         ull h[kStCount];
         CK(cudaMemcpy(h, v->d_stats, sizeof h, cudaMemcpyDeviceToHost));
-        h[kStSaturated] = sat;
+        h[kStSaturated] = std::max<ull>(h[kStSaturated], sat);
         CK(cudaMemcpy(v->d_stats, h, sizeof h, cudaMemcpyHostToDevice));
     }
     return SVR_OK;
@@ -1685,6 +1686,8 @@ extern "C" int svr_write_accumulators(svr_volume* v, const svr_box* box, const u
     k_write_acc<<<(unsigned)((n + 255) / 256), 256, 0, v->stream>>>(v->acc, dev_grid(v->d), b, ts, tc);
     v->launches++;
     CKL();
+    // the fill layer is derived from the accumulators: stale now, so cleared (re-run fill_holes)
+    CK(cudaMemsetAsync(v->fill, 0, sizeof(uint32_t) * v->nvox, v->stream));
     CK(cudaFreeAsync(ts, v->stream));
     CK(cudaFreeAsync(tc, v->stream));
     CK(cudaStreamSynchronize(v->stream));

@@ -248,16 +248,21 @@ class VoxelGrid:
         d = self.desc
         np.savez_compressed(path, sum=s, count=c, dims=np.array([d.nx, d.ny, d.nz]),
                             voxel_mm=d.voxel_mm, origin=np.array(list(d.origin_mm)),
-                            z_range=np.array([d.z_begin, d.z_end]))
+                            z_range=np.array([d.z_begin, d.z_end]),
+                            frames_inserted=self.stats()["frames_inserted"])
 
     def load(self, path):
-        """Resume from `save`: the grid description must match."""
+        """Resume from `save`: the grid description (dims, slab, voxel size, origin) must match.
+        The fill layer is derived state and is cleared (re-run fill_holes); the checkpoint's
+        frames_inserted is returned (device stats count only this handle's own inserts)."""
         z = np.load(path)
         d = self.desc
         if list(z["dims"]) != [d.nx, d.ny, d.nz] or list(z["z_range"]) != [d.z_begin, d.z_end] or \
-                float(z["voxel_mm"]) != d.voxel_mm:
+                float(z["voxel_mm"]) != d.voxel_mm or \
+                not np.array_equal(np.asarray(z["origin"], np.float64), np.array(list(d.origin_mm), np.float64)):
             raise InvalidInput("checkpoint does not match this grid")
         self.set_accumulators(z["sum"], z["count"])
+        return int(z["frames_inserted"]) if "frames_inserted" in z else None
 
     def values(self, box=None, apply_fills=False):
         """VoxelGrid::value (SPEC.md:277) = round(sum/count), 0 when empty."""

@@ -619,13 +619,18 @@ def test_checkpoint_resume(tmp_path):
     a.insert_frames(frames[:17], wl.poses[:17], wl.calib)
     a.save(tmp_path / "ck.npz")
     b = _grid(wl)
-    b.load(tmp_path / "ck.npz")
+    b.fill_holes(None, 1, pkg.FILL_MEAN)
+    assert b.load(tmp_path / "ck.npz") == 17  # frames_inserted of the checkpoint
+    assert not b.fill_layer().any()  # the derived fill layer is cleared on restore
     b.insert_frames(frames[17:], wl.poses[17:], wl.calib)
     for x, y in zip(b.accumulators(), full.accumulators()):
         assert np.array_equal(x, y)
     other = pkg.VoxelGrid((8, 8, 8), 1.0, (0, 0, 0), device=0)
     with pytest.raises(pkg.InvalidInput):
         other.load(tmp_path / "ck.npz")
+    shifted = pkg.VoxelGrid(wl.dims, wl.voxel_mm, (wl.origin[0] + 1.0, wl.origin[1], wl.origin[2]), device=0)
+    with pytest.raises(pkg.InvalidInput):  # same dims, different origin: refused
+        shifted.load(tmp_path / "ck.npz")
 
 
 @pytest.mark.parametrize("groups", [3, 8])
