@@ -1008,14 +1008,24 @@ static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
     return SVR_OK;
 }
 
-constexpr int kLinSmall = 4;  // launches of <= 4 frames (the per-frame path) prefer 32-column tiles
-
-static int pick_shape(int shapes, int w, int nframes, int small) {
-    static const int big_pref[4] = {0, 1, 2, 3}, small_pref[4] = {1, 3, 0, 2};
-    const int* pref = nframes <= small ? small_pref : big_pref;
-    for (int i = 0; i < 4; ++i)
-        if (((shapes >> pref[i]) & 1) && w % shape_cols(pref[i]) == 0) return pref[i];
-    return -1;
+// Tile shape for a launch: the least per-thread work on the critical path -- ceil(tiles /
+// resident CTAs) rounds, each a row of TCOLS pixels per thread -- with the 64 x 128 shape (the
+// fewest table positions per pixel) preferred within 5%.  Resident CTAs per SM: SVR_TILES_MINB
+// for the 128-thread shapes, twice that for the 64-thread ones (register-bound).
+static int pick_shape(int shapes, int w, int h, int nframes, int num_sms) {
+    int best = -1;
+    double best_cost = 0;
+    for (int sh = 0; sh < 4; ++sh) {
+        if (!((shapes >> sh) & 1) || w % shape_cols(sh)) continue;
+        const double tiles = (double)nframes * (w / shape_cols(sh)) * ((h + shape_rows(sh) - 1) / shape_rows(sh));
+        const double slots = (double)num_sms * (shape_rows(sh) == 128 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB);
+        const double cost = std::ceil(tiles / slots) * shape_cols(sh) * (1.0 + 0.05 * (sh != 0));
+        if (best < 0 || cost < best_cost) {
+            best = sh;
+            best_cost = cost;
+        }
+    }
+    return best;
 }
 
 static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, long long pitch,
@@ -1065,7 +1075,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     // linear probes: k_pnn_tiles (reads each row segment with 32-byte loads)
     const bool vec32 = ((uintptr_t)px % 32 == 0) && (pitch % 32 == 0) && (n == 1 || fstride % 32 == 0);
     const int shape = (mode == kModeInsert && !skip && !direct && cal.probe == SVR_PROBE_LINEAR && vec32)
-                          ? pick_shape(v->lin_shapes_cur, w, n, kLinSmall)
+                          ? pick_shape(v->lin_shapes_cur, w, h, n, v->num_sms)
                           : -1;
     // convex fan: k_pnn_plane's 64 x 64-sample tiles (table only where the tile's extent fits) + the
     // exact pass.  Its packed (count << 20 | sum) slot holds at most 4095 pixels: guaranteed when
@@ -1990,7 +2000,7 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm) || !shape_ok) {
         v->lin_shapes_cur = fpar.lin_fit;
         if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;
-        f.shape = pick_shape(fpar.lin_fit, w, 1, kLinSmall);
+        f.shape = pick_shape(fpar.lin_fit, w, h, 1, v->num_sms);
         ++f.captures;
     }
     *f.h_fp = fpar;
