@@ -18,6 +18,7 @@
 #include "svr_host.hpp"
 #include "svr_kernels.cuh"
 #include "svr_k1.cuh"
+#include "svr_fan.cuh"
 
 using namespace svr;
 
@@ -131,7 +132,7 @@ struct svr_volume {
     double fan_angle = 0.0;
     uint64_t launches = 0;
     uint64_t frames = 0;
-    ull* d_work = nullptr;          // deferred exact-path chunks of k_pnn_plane
+    ull* d_work = nullptr;          // deferred exact-path chunks (k_pnn_tiles / k_fan_tiles / k_pnn_plane)
     FrameGraph fg;                  // svr_frame_step graph
     GatherTargets gt{nullptr, 0, 0, 0, 0};  // fused render + gather targets (device pointer array)
     float** d_gt = nullptr;
@@ -154,6 +155,11 @@ struct svr_volume {
     TileDesc* d_desc = nullptr; // k_pnn_tiles per-tile descriptors
     long long desc_cap = 0;
     int num_sms = 148;          // the device's SM count (grid sizing)
+    FanDesc* d_fdesc = nullptr; // k_fan_tiles per-tile descriptors
+    long long fdesc_cap = 0;
+    FanRow* d_frows = nullptr;  // k_fan_tiles per-scanline constants
+    long long frows_cap = 0;
+    int fan_occ[2] = {0, 0};    // k_fan_tiles resident CTAs per SM, per <box> (lazy)
     int fill_mode = SVR_FILL_MEAN;  // mode of the latest fill_holes: decodes the fill layer on readout
 };
 
@@ -709,6 +715,8 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
     cudaFree(v->d_desc);
+    cudaFree(v->d_fdesc);
+    cudaFree(v->d_frows);
     cudaFree(v->d_work);
     for (int i = 0; i < svr_volume::kTileSlots; ++i) {
         cudaFree(v->d_tiles[i]);
@@ -992,6 +1000,71 @@ static int ensure_desc(svr_volume* v, long long ntiles) {
     return SVR_OK;
 }
 
+// k_fan_tiles buffers (grown outside any graph capture: fg_capture pre-sizes them)
+static int ensure_fan_bufs(svr_volume* v, long long ntiles, long long nrows) {
+    if (v->fdesc_cap < ntiles) {
+        CK(cudaStreamSynchronize(v->stream));
+        cudaFree(v->d_fdesc);
+        v->d_fdesc = nullptr;
+        v->fdesc_cap = std::max<long long>(ntiles, 4096);
+        CK(cudaMalloc(&v->d_fdesc, sizeof(FanDesc) * v->fdesc_cap));
+    }
+    if (v->frows_cap < nrows) {
+        CK(cudaStreamSynchronize(v->stream));
+        cudaFree(v->d_frows);
+        v->d_frows = nullptr;
+        v->frows_cap = std::max<long long>(nrows, 4096);
+        CK(cudaMalloc(&v->d_frows, sizeof(FanRow) * v->frows_cap));
+    }
+    return SVR_OK;
+}
+
+// K1 for convex probes: k_fan_desc (scanline constants + tile descriptors), k_fan_tiles
+// (persistent over the launch's tiles); the caller launches the exact pass.
+static int launch_fan(svr_volume* v, bool box, const uint8_t* px, long long pitch, long long fstride,
+                      int w, int h, int m, const FrameParams* fps, const DevCalib& cal, int* boxes,
+                      ull* stats) {
+    constexpr int TCOLS = 128;
+    FanArgs fa;
+    fa.px = px;
+    fa.pitch = pitch;
+    fa.fstride = fstride;
+    fa.w = w;
+    fa.h = h;
+    fa.ntx = w / TCOLS;
+    fa.nty = (h + kFanLines - 1) / kFanLines;
+    fa.ntiles = (long long)m * fa.ntx * fa.nty;
+    fa.fps = fps;
+    fa.cal = cal;
+    fa.fan = v->d_fan;
+    fa.g = dev_grid(v->d);
+    fa.acc = v->acc;
+    fa.boxes = boxes;
+    fa.stats = stats;
+    fa.work = v->d_work;
+    fa.work_n = v->d_work_n;
+    fa.work_cap = v->work_cap;
+    // table mode when the tile's index box has at most one position per pixel (A/B on cfg3:
+    // thresholds 1/4 .. 2 px per position within 1%)
+    fa.dense = 4;
+    if (int e = ensure_fan_bufs(v, fa.ntiles, (long long)m * h)) return e;
+    fa.desc = v->d_fdesc;
+    fa.rows = v->d_frows;
+    const int slot = box ? 1 : 0;
+    if (!v->fan_occ[slot]) {
+        int occ = 0;
+        if (box) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fan_tiles<true>, 128, 0));
+        else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fan_tiles<false>, 128, 0));
+        v->fan_occ[slot] = std::max(1, occ);
+    }
+    const long long ctas = std::min<long long>(fa.ntiles, (long long)v->num_sms * v->fan_occ[slot]);
+    k_fan_desc<TCOLS><<<(unsigned)((fa.ntiles * 32 + 127) / 128), 128, 0, v->stream>>>(fa);
+    if (box) k_fan_tiles<true><<<(unsigned)ctas, 128, 0, v->stream>>>(fa);
+    else k_fan_tiles<false><<<(unsigned)ctas, 128, 0, v->stream>>>(fa);
+    v->launches += 2;
+    return SVR_OK;
+}
+
 // K1 for linear probes: k_pnn_tiles (persistent over the launch's tiles) + the exact pass.
 template <int NCH, int NW, bool kBox>
 static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
@@ -1062,9 +1135,10 @@ static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, l
 }
 
 // Launch over frames resident in device memory, chunked to the grid.y limit.
-//   PNN insert: k_pnn_plane + k_pnn_work (default, when tile_ok and no skip_zero), k_insert
-//   direct (SVR_INSERT_KERNEL=direct, skip_zero, narrow tiles), k_pnn_rows (=rows),
-//   k_pnn_tile (SVR_INSERT_KERNEL=tile, when tile_ok); footprint / trilinear: k_insert.
+//   PNN insert, no skip_zero: linear probes k_tile_desc + k_pnn_tiles (svr_k1.cuh); convex fans
+//   k_fan_desc + k_fan_tiles (svr_fan.cuh, 32-byte aligned rows of whole 128-sample tiles) or
+//   else k_pnn_plane; each + k_pnn_work (the exact pass).  k_insert: skip_zero, geometries the
+//   tiles refuse, SVR_INSERT_KERNEL=direct (tests), footprint and trilinear.
 static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long pitch,
                          long long fstride, int w, int h, int n, const FrameParams* fps,
                          const DevCalib& cal, bool skip, bool box, int* boxes, uint32_t* mark,
@@ -1077,12 +1151,14 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     const int shape = (mode == kModeInsert && !skip && !direct && cal.probe == SVR_PROBE_LINEAR && vec32)
                           ? pick_shape(v->lin_shapes_cur, w, h, n, v->num_sms)
                           : -1;
-    // convex fan: k_pnn_plane's 64 x 64-sample tiles (table only where the tile's extent fits) + the
-    // exact pass.  Its packed (count << 20 | sum) slot holds at most 4095 pixels: guaranteed when
-    // every tile has two samples more than a voxel diagonal apart (63 dr > sqrt(3) voxel)
+    // convex fan: tables of packed (count << 20 | sum) slots hold at most 4095 pixels: guaranteed
+    // when samples 63 apart are more than a voxel diagonal apart (63 dr > sqrt(3) voxel: at most
+    // 63 samples of a scanline per voxel, 32 scanlines per k_fan_tiles tile, 64 per k_pnn_plane)
     const bool fan_plane = mode == kModeInsert && !skip && !direct && cal.probe == SVR_PROBE_FAN &&
                            w >= 4 * kChunk && (long long)v->d.nx * v->d.ny < (1ll << 22) &&
                            63.0 * cal.dr > std::sqrt(3.0) * v->d.voxel_mm;
+    // convex fan with 32-byte aligned rows of whole 128-sample tiles: k_fan_tiles
+    const bool fan_tiles = fan_plane && vec32 && w % 128 == 0;
     for (int k0 = 0; k0 < n; k0 += 65535) {
         int m = std::min(65535, n - k0);
         const uint8_t* p = px + (long long)k0 * fstride;
@@ -1091,8 +1167,8 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
         // a single frame must not pay for launching thousands of idle CTAs
         const int work_ctas = std::min(4096, std::max(16, 8 * m));
         const GridDev gd = dev_grid(v->d);
-        if (shape >= 0) {
-            // k_pnn_tiles defers whole chunks with no overflow path: room for every chunk
+        if (shape >= 0 || fan_tiles) {
+            // k_pnn_tiles / k_fan_tiles defer whole chunks with no overflow path: room for every chunk
             const long long need = std::max<long long>(1ll << 20, (long long)m * h * (w / kChunk));
             if (need > 0xffffffffll) return fail(SVR_E_INVALID, "insert batch too large");
             if (!v->d_work || v->work_cap < need) {
@@ -1104,7 +1180,11 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                 if (!v->d_work_n) CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
             }
             CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
-            if (int e = launch_tiles(v, shape, box, p, pitch, fstride, w, h, m, fps + k0, bx, stats)) return e;
+            if (fan_tiles) {
+                if (int e = launch_fan(v, box, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats)) return e;
+            } else {
+                if (int e = launch_tiles(v, shape, box, p, pitch, fstride, w, h, m, fps + k0, bx, stats)) return e;
+            }
             if (box)
                 k_pnn_work<true, true><<<work_ctas, 256, 0, v->stream>>>(
                     p, pitch, fstride, w, fps + k0, cal, v->d_fan, gd, v->acc, bx, stats, v->d_work,
@@ -1191,8 +1271,7 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
         if (int e = make_params(poses[k], ctx, c->scale_x_mm, c->scale_y_mm, &hp[k]))
             return fail(e, "frame %d: %s", k, g_err.c_str());
     if (int e = ensure_fan(v, *c)) return e;
-    // k_pnn_plane tile width: 6 chunks (96 px) when every frame's tile stays within the 32 x 32
-    // voxel table (x extent over 96 columns + 64 rows, plus the +-1 margins), else 4
+    // k_pnn_tiles shapes every frame of the call fits (FrameParams::lin_fit)
     v->lin_shapes_cur = 0xf;
     for (int k = 0; k < n; ++k) v->lin_shapes_cur &= hp[k].lin_fit;
     CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
@@ -1914,6 +1993,8 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
     }
     if (int e = ensure_fan(v, c)) return e;
     if (int e = ensure_desc(v, (long long)(w / 32 + 1) * (h / 64 + 1))) return e;
+    if (c.probe == SVR_PROBE_FAN)
+        if (int e = ensure_fan_bufs(v, (long long)(w / 128 + 1) * (h / kFanLines + 1), h)) return e;
     // bounds with headroom: later frames of a sweep rarely need a larger graph
     f.fill_ctas = std::max(f.fill_ctas, nf + nf / 4 + 1);
     f.depth_ctas = std::max(f.depth_ctas, nd + nd / 4 + 1);

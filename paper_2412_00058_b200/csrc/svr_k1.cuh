@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             int Sn, rown, rowcn;
             bool actn;
             tile_rows(ty, Sn, rown, actn, rowcn);
+            wait_desc();  // (before the row load: the wait would also cover it)
             load_rows(f, tx, rowcn, wd);
-            wait_desc();
         }
         __syncthreads();  // table complete
         if (tok) {

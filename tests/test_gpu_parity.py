@@ -115,6 +115,25 @@ def test_fan_bitexact():
     assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
 
 
+@pytest.mark.parametrize("z_range", [None, (12, 30)])
+def test_fan_tiles_bitexact(z_range):
+    """k_fan_tiles (fan frames of whole 128-sample tiles): 40 scanlines (a short last tile of 8),
+    dense table tiles near the apex and direct-run tiles far out, frames leaving the grid, and a
+    slab whose faces cut the frames (face tiles: per-chunk classes and the exact pass)."""
+    wl = synth.small_fan(nframes=12, lines=40, samples=256)
+    frames = wl.frames_np()
+    grid = pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, device=0, z_range=z_range)
+    boxes, _ = grid.insert_frames(frames, wl.poses, wl.calib, want_boxes=True)
+    ref = O.OracleGrid(wl.dims, wl.voxel_mm, wl.origin, z_range=z_range)
+    rboxes = ref.insert_frames(frames, wl.poses, wl.calib)
+    _assert_acc(grid, ref)
+    assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
+    st = grid.stats()
+    assert st["pixels_inserted"] == ref.stats["inserted"] and st["pixels_oob"] == ref.stats["oob"]
+    assert st["tiles_table"] == wl.nframes * 2 * 2  # every tile through k_fan_tiles
+    grid.close()
+
+
 def test_cfg3_fan_subset_bitexact():
     wl = synth.cfg3()
     idx = np.arange(0, wl.nframes, 45)  # 40 frames spread over the sweep

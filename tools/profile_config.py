@@ -1,0 +1,35 @@
+#!/usr/bin/env python
+"""Insert-only launches of one BASELINE config (device-resident frames) for ncu: cfg1 / cfg3 /
+cfg5 (cfg5 on a 64-plane slab so it fits beside other processes).  usage: profile_config.py NAME [STEPS]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2412_00058_b200 as pkg  # noqa: E402
+from paper_2412_00058_b200 import sharding, synth  # noqa: E402
+
+name = sys.argv[1]
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+wl = synth.CONFIGS[name]()
+z_range, poses, idx = None, wl.poses, None
+if name == "cfg5":
+    z_range = (1200, 1264)
+    boxes = sharding.frame_boxes(wl.grid_desc(), wl.calib, wl.poses)
+    idx = sharding.route(boxes, z_range)
+    poses = wl.poses[idx]
+n = len(poses)
+frames = torch.empty((n, wl.h, wl.w), dtype=torch.uint8, device="cuda")
+if idx is None:
+    synth.synth_frames_device(wl, frames, 0, n)
+else:
+    for i, k in enumerate(idx):
+        synth.synth_frames_device(wl, frames[i:i + 1], int(k), 1)
+grid = pkg.VoxelGrid(wl.dims, wl.voxel_mm, wl.origin, z_range=z_range, accum=wl.accum)
+for _ in range(steps):
+    grid.insert_frames(frames, poses, wl.calib)
+grid.sync()
+print("ok", name, n, grid.stats())

@@ -4,6 +4,8 @@
 //   atoms32_spread : shared-memory atomicAdd (u32) to pseudo-random slots of a 16 KiB table
 //   atoms32_run    : shared atomics, 4 lanes per address
 //   sts32_spread   : plain shared stores, same pattern (LSU reference)
+//   red64_256MiB   : RED.64 spread over 256 MiB (DRAM read-modify-write)
+//   red64_warp64w  : a warp's lanes within 64 words of a random per-warp base, 256 MiB window
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_atomics tools/ubench_atomics.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -27,6 +29,9 @@ __global__ void __launch_bounds__(256) kern(unsigned long long* g, int iters, un
         if (MODE == 4) s[key & 4095] = key;
         if (MODE == 5) atomicAdd(&g[(key % 30000u) * 7u % (1u << 17)], 1ull);  // hot 30k-address set
         if (MODE == 6) atomicAdd(&g[(t >> 3) % 30000u], 1ull);                  // 8 lanes/address
+        if (MODE == 7) atomicAdd(&g[key & ((1u << 25) - 1)], 1ull);             // 256 MiB window
+        if (MODE == 8)  // warp-local: lanes within 64 words of a per-warp random base (sector sharing)
+            atomicAdd(&g[((hash32((t >> 5) * 31u + it) & ((1u << 25) - 1)) + (hash32(t + it) & 63u)) & ((1u << 25) - 1)], 1ull);
     }
     __syncthreads();
     if (MODE >= 2 && threadIdx.x == 0) sink[blockIdx.x] = s[lane];
@@ -51,9 +56,9 @@ float run(const char* name, unsigned long long* g, unsigned long long* sink, int
 
 int main() {
     unsigned long long *g, *sink;
-    cudaMalloc(&g, sizeof(unsigned long long) << 17);
+    cudaMalloc(&g, sizeof(unsigned long long) << 25);
     cudaMalloc(&sink, sizeof(unsigned long long) << 20);
-    cudaMemset(g, 0, sizeof(unsigned long long) << 17);
+    cudaMemset(g, 0, sizeof(unsigned long long) << 25);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     int blocks = sms * 8, iters = 512;
@@ -64,6 +69,8 @@ int main() {
     run<4>("sts32_spread", g, sink, blocks, iters);
     run<5>("red64_hot30k", g, sink, blocks, iters);
     run<6>("red64_same8", g, sink, blocks, iters);
+    run<7>("red64_256MiB", g, sink, blocks, iters);
+    run<8>("red64_warp64w", g, sink, blocks, iters);
     cudaError_t e = cudaDeviceSynchronize();
     printf("status %s, SMs %d\n", cudaGetErrorString(e), sms);
     return e == cudaSuccess ? 0 : 1;
