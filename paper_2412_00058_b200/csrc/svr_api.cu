@@ -154,6 +154,8 @@ struct svr_volume {
     int tiles_occ[8] = {0};     // k_pnn_tiles resident CTAs per SM, per <shape, box> (lazy)
     TileDesc* d_desc = nullptr; // k_pnn_tiles per-tile descriptors
     long long desc_cap = 0;
+    TileFrame* d_frc = nullptr; // k_pnn_tiles per-frame constants
+    long long frc_cap = 0;
     int num_sms = 148;          // the device's SM count (grid sizing)
     FanDesc* d_fdesc = nullptr; // k_fan_tiles per-tile descriptors
     long long fdesc_cap = 0;
@@ -715,6 +717,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFreeHost(v->h_boxes);
     cudaFree(v->d_fan);
     cudaFree(v->d_desc);
+    cudaFree(v->d_frc);
     cudaFree(v->d_fdesc);
     cudaFree(v->d_frows);
     cudaFree(v->d_work);
@@ -990,13 +993,21 @@ static bool is_device_ptr(const void* p, bool* pinned) {
 
 // per-tile descriptor buffer of k_pnn_tiles (grown outside any graph capture: fg_capture
 // pre-sizes it for one frame)
-static int ensure_desc(svr_volume* v, long long ntiles) {
-    if (v->desc_cap >= ntiles) return SVR_OK;
-    CK(cudaStreamSynchronize(v->stream));
-    cudaFree(v->d_desc);
-    v->d_desc = nullptr;
-    v->desc_cap = std::max<long long>(ntiles, 4096);
-    CK(cudaMalloc(&v->d_desc, sizeof(TileDesc) * v->desc_cap));
+static int ensure_desc(svr_volume* v, long long ntiles, long long nframes) {
+    if (v->desc_cap < ntiles) {
+        CK(cudaStreamSynchronize(v->stream));
+        cudaFree(v->d_desc);
+        v->d_desc = nullptr;
+        v->desc_cap = std::max<long long>(ntiles, 4096);
+        CK(cudaMalloc(&v->d_desc, sizeof(TileDesc) * v->desc_cap));
+    }
+    if (v->frc_cap < nframes) {
+        CK(cudaStreamSynchronize(v->stream));
+        cudaFree(v->d_frc);
+        v->d_frc = nullptr;
+        v->frc_cap = std::max<long long>(nframes, 256);
+        CK(cudaMalloc(&v->d_frc, sizeof(TileFrame) * v->frc_cap));
+    }
     return SVR_OK;
 }
 
@@ -1120,8 +1131,9 @@ static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, l
     ta.work = v->d_work;
     ta.work_n = v->d_work_n;
     ta.work_cap = v->work_cap;
-    if (int e = ensure_desc(v, ta.ntiles)) return e;
+    if (int e = ensure_desc(v, ta.ntiles, m)) return e;
     ta.desc = v->d_desc;
+    ta.frc = v->d_frc;
     switch (shape + 4 * box) {
         case 0: return launch_tiles_t<4, 4, false>(v, ta);
         case 1: return launch_tiles_t<2, 4, false>(v, ta);
@@ -1992,7 +2004,7 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
         CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
     }
     if (int e = ensure_fan(v, c)) return e;
-    if (int e = ensure_desc(v, (long long)(w / 32 + 1) * (h / 64 + 1))) return e;
+    if (int e = ensure_desc(v, (long long)(w / 32 + 1) * (h / 64 + 1), 1)) return e;
     if (c.probe == SVR_PROBE_FAN)
         if (int e = ensure_fan_bufs(v, (long long)(w / 128 + 1) * (h / kFanLines + 1), h)) return e;
     // bounds with headroom: later frames of a sweep rarely need a larger graph

@@ -1,9 +1,12 @@
 // svr_k1.cuh — K1, the pixel-nearest-neighbour insert of linear-probe B-scans,
 // as a persistent tile kernel.  Included by svr_api.cu after svr_kernels.cuh.
 //
-// Work unit: a tile of TCOLS = 16*NCH columns x TROWS = 32*NW rows of one frame.  Each CTA walks a
-// contiguous range of the launch's tiles (frame-major), so a frame's constants are loaded once per
-// ~30 tiles and the last wave is one tile long.
+// Work unit: a tile of TCOLS = 16*NCH columns x TROWS = 32*NW rows of one frame.  The tiles
+// (frame-major) go round-robin over persistent CTAs, so the CTAs in flight together cover a
+// window of ~grid consecutive tiles: neighbouring frames' adds to the same voxels meet in L2 (a
+// CTA walking a contiguous range instead spread them over the whole launch: 76% of the REDs'
+// sectors missed L2, profiles/r2_opt_log.md).  Each tile's descriptor and frame constants are
+// staged with cp.async two tiles ahead.
 //
 // Lane map: thread (warp w, lane l) walks the whole TCOLS-pixel row r = w + NW*l of the tile.  The
 // 32 lanes of a warp then sit on rows NW apart (cfg2: 1.67 voxels apart in y), so one shared
@@ -59,6 +62,7 @@ struct TilesArgs {
     unsigned int* work_n;
     unsigned int work_cap;
     const struct TileDesc* desc;  // per-tile constants (k_tile_desc)
+    struct TileFrame* frc;        // per-frame constants (k_tile_desc)
 };
 
 // Per-tile constants, computed once per tile by k_tile_desc instead of redundantly by every warp
@@ -88,14 +92,16 @@ __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& 
         : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy));
 }
 
-// A frame's constants, staged in shared memory when a CTA's tile range enters the frame (keeps
-// the 64-register budget for the walk).
-struct TileFrame {
+// A frame's constants (k_tile_desc writes one per frame), staged in shared memory with each
+// tile's descriptor (keeps the 64-register budget for the walk).
+struct __align__(16) TileFrame {
     long long Dc[3], Dr[3];        // 32.32 fixed: du/dcol, du/drow
     uint32_t E[3], neg[3];         // |Dc| low words; all-ones when Dc < 0 (mirrored fractions)
     uint32_t te2, sx, sy;          // tie window + 1; table byte steps along x and y
     float p1, p2;                  // frame plane slopes (FrameParams::pz[1], pz[2])
+    uint32_t pad;
 };
+static_assert(sizeof(TileFrame) == 96, "TileFrame is staged as 6 x 16 bytes");
 
 __device__ __forceinline__ void push_work(const TilesArgs& ta, int f, int row, int cc) {
     // the host sizes the list for every chunk of the launch, so it cannot overflow
@@ -151,6 +157,24 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
     d.base = 8ll * ((long long)(zint + kmin - g.zb) * sxy + (long long)lo[1] * g.nx + lo[0]);
     d.pad[0] = d.pad[1] = 0;
     out[t] = d;
+    if (rem == 0) {  // the frame's constants, once
+        TileFrame fr;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const long long dc = fp.Dc[k];
+            fr.Dc[k] = dc;
+            fr.Dr[k] = fp.Dr[k];
+            fr.E[k] = (uint32_t)(dc < 0 ? -dc : dc);
+            fr.neg[k] = dc < 0 ? 0xffffffffu : 0u;
+        }
+        fr.te2 = fp.tie_eps + 1;
+        fr.sx = fp.Dc[0] < 0 ? 0u - 4u : 4u;
+        fr.sy = fp.Dc[1] < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
+        fr.p1 = (float)fp.pz[1];
+        fr.p2 = (float)fp.pz[2];
+        fr.pad = 0u;
+        ta.frc[f] = fr;
+    }
 }
 
 // Walk state (fractions + table byte address) of the pixel whose fixed-point u is (u0, u1, u2).
@@ -192,10 +216,10 @@ template <int NCH, int NW, bool kBox>
 __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB) k_pnn_tiles(const TilesArgs ta) {
     constexpr int NT = 32 * NW, TROWS = 32 * NW, TCOLS = 16 * NCH;
     __shared__ __align__(16) uint32_t s_tab[kTabWords];
-    __shared__ TileFrame s_fr;
+    __shared__ TileFrame s_frs[3];       // ring (tiles i, i + 1, i + 2): frame constants
+    __shared__ TileDesc s_desc[3];       //   and descriptors, cp.async-staged
     __shared__ unsigned int s_cnt[2];    // chunks counted out of bounds / deferred (rare)
     __shared__ unsigned long long s_px;  // pixels of this CTA's tiles
-    __shared__ TileDesc s_desc[2];       // current / next tile's descriptor (cp.async-staged)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 2) s_cnt[tid] = 0u;
     if (tid == 0) s_px = 0ull;
@@ -206,12 +230,37 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
     const bool tab_ok = tab + 4u * 2048u <= 16384u;
     const GridDev& g = ta.g;
     const int tpf = ta.ntx * ta.nty;
-    const long long t0 = (long long)blockIdx.x * ta.ntiles / gridDim.x;
-    const long long t1 = (long long)(blockIdx.x + 1) * ta.ntiles / gridDim.x;
+    // tiles round-robin over the CTAs: the CTAs in flight together work on a window of ~grid
+    // consecutive tiles (a few dozen frames), so neighbouring frames' adds to the same voxels
+    // meet in L2 instead of each reading the voxel's sector from HBM
+    const long long t0 = blockIdx.x, tstep = gridDim.x, t1 = ta.ntiles;
+    __shared__ int s_adv[3];  // tstep as (frames, tile rows, tile columns)
+    if (tid == 0) {
+        const int sf = (int)(tstep / tpf), sr = (int)(tstep - (long long)sf * tpf);
+        s_adv[0] = sf;
+        s_adv[1] = sr / ta.ntx;
+        s_adv[2] = sr - s_adv[1] * ta.ntx;
+    }
+    __syncthreads();
+    auto advance = [&](int& fq, int& tyq, int& txq) {  // tile + tstep, without divisions
+        txq += s_adv[2];
+        tyq += s_adv[1];
+        fq += s_adv[0];
+        if (txq >= ta.ntx) {
+            txq -= ta.ntx;
+            ++tyq;
+        }
+        if (tyq >= ta.nty) {
+            tyq -= ta.nty;
+            ++fq;
+        }
+    };
     int f = (int)(t0 / tpf);
     int rem = (int)(t0 - (long long)f * tpf);
     int ty = rem / ta.ntx, tx = rem - ty * ta.ntx;
     int cur_f = -1;
+    unsigned int ntiles_cta = 0;
+    int slot = 0;
     BoxAcc bb;
 
     // Rows of a short last tile go to whole warps (rows w + S l, S = active warps): an idle warp
@@ -223,61 +272,66 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         act = warp < S && row < ta.h;
         rowc = act ? row : ta.h - 1;
     };
-    // this thread's row of pixels (software-pipelined: the next tile's rows and descriptor are
-    // requested before the current tile's flush)
+    // this thread's row of pixels (software-pipelined: the next tile's rows are requested before
+    // the current tile's flush)
     uint32_t wd[NCH][4];
     auto load_rows = [&](int fq, int txq, int rowq, uint32_t (&d)[NCH][4]) {
         const uint8_t* src = ta.px + (long long)fq * ta.fstride + (long long)rowq * ta.pitch + txq * TCOLS;
 #pragma unroll
         for (int c = 0; c < NCH; c += 2) ld256(src + 16 * c, &d[c][0]);
     };
-    // threads 0..3 stage a tile descriptor (4 x 16 B) into shared memory with cp.async
-    auto stage_desc = [&](long long t, int b) {
+    // threads 0..3 stage a tile's descriptor (4 x 16 B), 4..9 its frame's constants (6 x 16 B);
+    // one commit group per tile (empty for the other threads): waiting for all but the newest
+    // group leaves the tile two ahead in flight
+    auto stage = [&](int fq, int tyq, int txq, int b) {
+        const long long t = (long long)fq * tpf + tyq * ta.ntx + txq;
         if (tid < 4) {
             const uint32_t dst = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4*>(&s_desc[b]) + tid);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                          "l"(reinterpret_cast<const uint4*>(ta.desc + t) + tid) : "memory");
+        } else if (tid < 10) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4*>(&s_frs[b]) + (tid - 4));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(reinterpret_cast<const uint4*>(ta.frc + fq) + (tid - 4)) : "memory");
         }
     };
-    auto wait_desc = [&]() {
-        if (tid < 4) asm volatile("cp.async.wait_all;" ::: "memory");
-    };
+    auto commit = [&]() { asm volatile("cp.async.commit_group;" ::: "memory"); };
+    auto wait_stage = [&]() { asm volatile("cp.async.wait_group 1;" ::: "memory"); };
     if (t0 < t1) {
         int S, row, rowc;
         bool act;
         tile_rows(ty, S, row, act, rowc);
         load_rows(f, tx, rowc, wd);
-        stage_desc(t0, 0);
-        wait_desc();
+        stage(f, ty, tx, 0);
+        commit();
+        int f1 = f, ty1 = ty, tx1 = tx;
+        advance(f1, ty1, tx1);
+        if (t0 + tstep < t1) stage(f1, ty1, tx1, 1);
+        commit();
+        wait_stage();
     }
 
-    for (long long t = t0; t < t1; ++t) {
-        if (f != cur_f) {  // CTA-uniform
-            if (kBox && cur_f >= 0) {
+    for (long long t = t0; t < t1; t += tstep) {
+        if (kBox && f != cur_f) {  // CTA-uniform
+            if (cur_f >= 0) {
                 flush_box(bb, ta.boxes + 6 * cur_f);
                 bb = BoxAcc();
             }
             cur_f = f;
-            if (tid < 3) {
-                const FrameParams& fp = ta.fps[f];
-                const int k = tid;
-                const long long dc = fp.Dc[k];
-                s_fr.Dc[k] = dc;
-                s_fr.Dr[k] = fp.Dr[k];
-                s_fr.E[k] = (uint32_t)(dc < 0 ? -dc : dc);
-                s_fr.neg[k] = dc < 0 ? 0xffffffffu : 0u;
-                if (k == 0) {
-                    s_fr.te2 = fp.tie_eps + 1;
-                    s_fr.sx = dc < 0 ? 0u - 4u : 4u;
-                    s_fr.p1 = (float)fp.pz[1];
-                    s_fr.p2 = (float)fp.pz[2];
-                }
-                if (k == 1) s_fr.sy = dc < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
-            }
         }
         __syncthreads();  // frame constants + descriptor staged; table zeroed or flushed
-        const TileDesc& dsc = s_desc[(int)(t - t0) & 1];
-        if (t + 1 < t1) stage_desc(t + 1, (int)(t + 1 - t0) & 1);
+        const int b = slot;
+        slot = slot == 2 ? 0 : slot + 1;
+        ++ntiles_cta;
+        {  // the tile after next is requested now
+            int f2 = f, ty2 = ty, tx2 = tx;
+            advance(f2, ty2, tx2);
+            advance(f2, ty2, tx2);
+            if (t + 2 * tstep < t1) stage(f2, ty2, tx2, b == 0 ? 2 : b - 1);
+            commit();
+        }
+        const TileFrame& s_fr = s_frs[b];
+        const TileDesc& dsc = s_desc[b];
         const int c0t = tx * TCOLS, r0t = ty * TROWS;
         const int X0 = dsc.X0, Y0 = dsc.Y0, X = dsc.XY & 0xffff, Y = dsc.XY >> 16;
         const bool tok = (dsc.flags & 1) && tab_ok, tin = dsc.flags & 2;
@@ -382,18 +436,12 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         const unsigned long long fbase = (unsigned long long)ta.acc + (unsigned long long)dsc.base;
         const uint32_t zpar = (uint32_t)dsc.zpar;
         const float tt0 = dsc.tt0;
-        if (++tx == ta.ntx) {
-            tx = 0;
-            if (++ty == ta.nty) {
-                ty = 0;
-                ++f;
-            }
-        }
-        if (t + 1 < t1) {
+        advance(f, ty, tx);
+        wait_stage();  // (before the row load: the wait would also cover it)
+        if (t + tstep < t1) {
             int Sn, rown, rowcn;
             bool actn;
             tile_rows(ty, Sn, rown, actn, rowcn);
-            wait_desc();  // (before the row load: the wait would also cover it)
             load_rows(f, tx, rowcn, wd);
         }
         __syncthreads();  // table complete
@@ -437,7 +485,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 }
             }
         }
-        __syncthreads();  // table clean, frame constants free for the next tile
+        // (the next tile's top barrier orders this flush before its walk and before the ring
+        // slot read here is staged again)
     }
     if (kBox && cur_f >= 0) flush_box(bb, ta.boxes + 6 * cur_f);
     if (tid == 0) {  // (after the loop's last barrier: s_cnt is final)
@@ -447,7 +496,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         if (n_px > oob + 16ull * def) atomicAdd(&ta.stats[kStInserted], n_px - oob - 16ull * def);
         if (oob) atomicAdd(&ta.stats[kStOob], oob);
         if (def) atomicAdd(&ta.stats[kStDeferred], def);
-        if (t1 > t0) atomicAdd(&ta.stats[kStTiles], (ull)(t1 - t0));
+        if (ntiles_cta) atomicAdd(&ta.stats[kStTiles], (ull)ntiles_cta);
     }
 }
 
