@@ -276,6 +276,9 @@ def measure_config(name, steps=3):
     if wl.accum == _abi.ACC_PNN:
         hbm, _ = _peaks()
         out["roofline_frac"] = alg / (ms / 1e3) / 1e9 / hbm
+        out["roofline_kernel"] = ("k_fan_desc + k_fan_tiles + k_pnn_work" if wl.calib.probe == _abi.PROBE_FAN
+                                  else "k_tile_desc + k_pnn_tiles + k_pnn_work")
+        out["bytes_model"] = "sum_f (W*H + 12*U_f), U_f distinct voxels of frame f"
         out["U_mean"] = float(U.mean())
     else:
         out.update(trilinear_extras(wl, grid, frames, stream, ms))
@@ -750,7 +753,7 @@ def run_ours(args):
                       "what": "insert-all / fill-all / render-all schedule, CUDA events per stage "
                               "(timed step: %d frame group(s))" % args.sweep_groups},
         "insert_only": {"value": total_px / ins_s / 1e9 if world == 1 else None, "unit": UNIT},
-        "roofline": {"bound": "hbm", "kernel": "k_pnn_lin + k_pnn_work (K1)", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "k_tile_desc + k_pnn_tiles + k_pnn_work (K1)", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,
