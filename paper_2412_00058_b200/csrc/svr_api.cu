@@ -151,7 +151,7 @@ struct svr_volume {
     int insert_kernel = 3;      // SVR_INSERT_KERNEL=direct: every PNN insert through k_insert (the
                                 // fallback kernel; tests use it to cover it on every geometry)
     int lin_shapes_cur = 0;     // k_pnn_tiles shapes every frame of the current insert call fits
-    int tiles_occ[8] = {0};     // k_pnn_tiles resident CTAs per SM, per <shape, box> (lazy)
+    int tiles_occ[16] = {0};    // k_pnn_tiles resident CTAs per SM, per <shape, box, z1> (lazy)
     TileDesc* d_desc = nullptr; // k_pnn_tiles per-tile descriptors
     long long desc_cap = 0;
     TileFrame* d_frc = nullptr; // k_pnn_tiles per-frame constants
@@ -284,7 +284,10 @@ struct PrepCtx {
     int lin_count_ok;  // tile shapes whose per-slot pixel count provably stays <= 4095
 };
 
-// k_pnn_tiles shapes (svr_k1.cuh): s = (NCH == 2) + 2 (NW == 2); columns 16 NCH x rows 32 NW
+// k_pnn_tiles shapes (svr_k1.cuh): s = (NCH == 2) + 2 (NW == 2); columns 16 NCH x rows 32 NW.
+// A launch's shape carries bit 2 (kShapeZ1) when every frame has at most one z carry per chunk
+// (FrameParams::lin_fit bit 4): the kZ1 walk variant.
+constexpr int kShapeZ1 = 4, kFitZ1 = 16;
 static inline int shape_cols(int s) { return (s & 1) ? 32 : 64; }
 static inline int shape_rows(int s) { return (s & 2) ? 64 : 128; }
 
@@ -301,7 +304,9 @@ static int tile_shapes_fit(const long long Dc[3], const long long Dr[3], int cou
         const double c1 = shape_cols(sh) - 1, r1 = shape_rows(sh) - 1;
         const double spx = (c1 * std::fabs((double)Dc[0]) + r1 * std::fabs((double)Dr[0])) * s;
         const double spy = (c1 * std::fabs((double)Dc[1]) + r1 * std::fabs((double)Dr[1])) * s;
-        if (std::floor(spx + 1e-9) + 2 <= 32 && std::floor(spy + 1e-9) + 2 <= 62) m |= 1 << sh;
+        // (table rows: 62 for 128-row tiles, 31 for 64-row ones: TabGeom in svr_k1.cuh)
+        const double ymax = shape_rows(sh) == 128 ? 62 : 31;
+        if (std::floor(spx + 1e-9) + 2 <= 32 && std::floor(spy + 1e-9) + 2 <= ymax) m |= 1 << sh;
     }
     return m;
 }
@@ -421,6 +426,8 @@ static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, doubl
         const double qp2 = pose.qw * pose.qw + pose.qx * pose.qx + pose.qy * pose.qy + pose.qz * pose.qz;
         if (fp->plane_ok && x.lin_ok && qp2 >= 0.98)  // (the count bound in prep_ctx assumes |q|^2 >= 0.98)
             fp->lin_fit = tile_shapes_fit(fp->Dc, fp->Dr, x.lin_count_ok);
+        // kZ1 walk: at most one z carry in the 15 steps of a 16-pixel chunk
+        if (fp->lin_fit && 15 * std::llabs(fp->Dc[2]) < (1ll << 32)) fp->lin_fit |= kFitZ1;
     }
     return SVR_OK;
 }
@@ -1077,17 +1084,17 @@ static int launch_fan(svr_volume* v, bool box, const uint8_t* px, long long pitc
 }
 
 // K1 for linear probes: k_pnn_tiles (persistent over the launch's tiles) + the exact pass.
-template <int NCH, int NW, bool kBox>
+template <int NCH, int NW, bool kBox, bool kZ1>
 static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
-    const int slot = (NCH == 2) + 2 * (NW == 2) + 4 * kBox;
+    const int slot = (NCH == 2) + 2 * (NW == 2) + 4 * kBox + 8 * kZ1;
     if (!v->tiles_occ[slot]) {
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pnn_tiles<NCH, NW, kBox>, 32 * NW, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pnn_tiles<NCH, NW, kBox, kZ1>, 32 * NW, 0));
         v->tiles_occ[slot] = std::max(1, occ);
     }
     const long long ctas = std::min<long long>(ta.ntiles, (long long)v->num_sms * v->tiles_occ[slot]);
-    k_tile_desc<NCH, NW><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->stream>>>(ta, const_cast<TileDesc*>(ta.desc));
-    k_pnn_tiles<NCH, NW, kBox><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
+    k_tile_desc<NCH, NW, kZ1><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->stream>>>(ta, const_cast<TileDesc*>(ta.desc));
+    k_pnn_tiles<NCH, NW, kBox, kZ1><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
     v->launches += 2;
     return SVR_OK;
 }
@@ -1103,13 +1110,16 @@ static int pick_shape(int shapes, int w, int h, int nframes, int num_sms) {
         if (!((shapes >> sh) & 1) || w % shape_cols(sh)) continue;
         const double tiles = (double)nframes * (w / shape_cols(sh)) * ((h + shape_rows(sh) - 1) / shape_rows(sh));
         const double slots = (double)num_sms * (shape_rows(sh) == 128 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB);
-        const double cost = std::ceil(tiles / slots) * shape_cols(sh) * (1.0 + 0.05 * (sh != 0));
+        double cost = std::ceil(tiles / slots) * shape_cols(sh) * (1.0 + 0.05 * (sh != 0));
+#ifdef SVR_TILES_SHAPE
+        if (sh == SVR_TILES_SHAPE) cost = 0;  // (A/B builds: force one shape where it fits)
+#endif
         if (best < 0 || cost < best_cost) {
             best = sh;
             best_cost = cost;
         }
     }
-    return best;
+    return best >= 0 && (shapes & kFitZ1) ? best | kShapeZ1 : best;
 }
 
 static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, long long pitch,
@@ -1134,15 +1144,23 @@ static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, l
     if (int e = ensure_desc(v, ta.ntiles, m)) return e;
     ta.desc = v->d_desc;
     ta.frc = v->d_frc;
-    switch (shape + 4 * box) {
-        case 0: return launch_tiles_t<4, 4, false>(v, ta);
-        case 1: return launch_tiles_t<2, 4, false>(v, ta);
-        case 2: return launch_tiles_t<4, 2, false>(v, ta);
-        case 3: return launch_tiles_t<2, 2, false>(v, ta);
-        case 4: return launch_tiles_t<4, 4, true>(v, ta);
-        case 5: return launch_tiles_t<2, 4, true>(v, ta);
-        case 6: return launch_tiles_t<4, 2, true>(v, ta);
-        default: return launch_tiles_t<2, 2, true>(v, ta);
+    switch ((shape & 7) + 8 * box) {
+        case 0: return launch_tiles_t<4, 4, false, false>(v, ta);
+        case 1: return launch_tiles_t<2, 4, false, false>(v, ta);
+        case 2: return launch_tiles_t<4, 2, false, false>(v, ta);
+        case 3: return launch_tiles_t<2, 2, false, false>(v, ta);
+        case 4: return launch_tiles_t<4, 4, false, true>(v, ta);
+        case 5: return launch_tiles_t<2, 4, false, true>(v, ta);
+        case 6: return launch_tiles_t<4, 2, false, true>(v, ta);
+        case 7: return launch_tiles_t<2, 2, false, true>(v, ta);
+        case 8: return launch_tiles_t<4, 4, true, false>(v, ta);
+        case 9: return launch_tiles_t<2, 4, true, false>(v, ta);
+        case 10: return launch_tiles_t<4, 2, true, false>(v, ta);
+        case 11: return launch_tiles_t<2, 2, true, false>(v, ta);
+        case 12: return launch_tiles_t<4, 4, true, true>(v, ta);
+        case 13: return launch_tiles_t<2, 4, true, true>(v, ta);
+        case 14: return launch_tiles_t<4, 2, true, true>(v, ta);
+        default: return launch_tiles_t<2, 2, true, true>(v, ta);
     }
 }
 
@@ -1284,7 +1302,7 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
             return fail(e, "frame %d: %s", k, g_err.c_str());
     if (int e = ensure_fan(v, *c)) return e;
     // k_pnn_tiles shapes every frame of the call fits (FrameParams::lin_fit)
-    v->lin_shapes_cur = 0xf;
+    v->lin_shapes_cur = 0xf | kFitZ1;
     for (int k = 0; k < n; ++k) v->lin_shapes_cur &= hp[k].lin_fit;
     CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
                        v->stream));
@@ -2089,7 +2107,9 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     if (int e = make_params(*pose, prep_ctx(*c, v->d), c->scale_x_mm, c->scale_y_mm, &fpar)) return e;
     // the insert's tile shape is part of the capture: a frame that fits none of the captured
     // shape's tiles is still exact (its tiles take the exact pass) but re-captures once
-    const bool shape_ok = f.shape < 0 ? fpar.lin_fit == 0 : ((fpar.lin_fit >> f.shape) & 1) != 0;
+    const bool shape_ok = f.shape < 0 ? fpar.lin_fit == 0
+                                      : ((fpar.lin_fit >> (f.shape & 3)) & 1) != 0 &&
+                                            (!(f.shape & kShapeZ1) || (fpar.lin_fit & kFitZ1));
     if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm) || !shape_ok) {
         v->lin_shapes_cur = fpar.lin_fit;
         if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;

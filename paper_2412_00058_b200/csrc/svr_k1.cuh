@@ -47,6 +47,17 @@ constexpr int kTabMaxY = 62;                   // voxel rows (62 * 33 <= 2048 wo
 constexpr int kTabMaxX = 32;                   // voxel columns
 constexpr int kTabWords = kTabPlane + 2048;    // 24 KB (the 8 KB gap is unused)
 
+// k_pnn_tiles table geometry per tile height: 128-row tiles (NW = 4) as above; 64-row tiles
+// (NW = 2) need at most 31 voxel rows, so plane 1 sits 8 KB up (bit 13) and the table is 12 KB --
+// small enough for 14 two-warp CTAs per SM (the same 28 warps, barriers over 2 warps instead of 4)
+template <int NW>
+struct TabGeom {
+    static constexpr int kBit = NW == 4 ? 16384 : 8192;  // byte distance of the parity planes
+    static constexpr int kPlane = kBit / 4;               // in words
+    static constexpr int kMaxY = NW == 4 ? 62 : 31;
+    static constexpr int kWords = kPlane + ((kMaxY * kTabStr + 3) & ~3);
+};
+
 struct TilesArgs {
     const uint8_t* px;
     long long pitch, fstride;
@@ -79,6 +90,7 @@ struct __align__(16) TileDesc {
 };
 
 // one exact step of the three fractions; the table byte address follows the carries
+template <int kBit = 16384>
 __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
                                           uint32_t e0, uint32_t e1, uint32_t e2, uint32_t sx,
                                           uint32_t sy) {
@@ -87,9 +99,25 @@ __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& 
         "add.cc.u32 %1, %1, %5;\n\taddc.u32 c1, 0, 0;\n\t"
         "add.cc.u32 %2, %2, %6;\n\taddc.u32 c2, 0, 0;\n\t"
         "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
-        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 xor.b32 %3, %3, 16384;\n\t}"
+        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 xor.b32 %3, %3, %9;\n\t}"
         : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a)
-        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy));
+        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "n"(kBit));
+}
+
+// tile_step for chunks with at most one z carry (kZ1): the z move is +-16 KB (dz, fixed per chunk
+// by its start parity) as a predicated add, which ptxas puts on the FMA pipe like the x and y
+// moves -- the walk is ALU-bound (carries, tie screen, PRMT), the FMA pipe had room
+__device__ __forceinline__ void tile_step_dz(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
+                                             uint32_t e0, uint32_t e1, uint32_t e2, uint32_t sx,
+                                             uint32_t sy, uint32_t dz) {
+    asm("{\n\t.reg .pred p0, p1, p2;\n\t.reg .u32 c0, c1, c2;\n\t"
+        "add.cc.u32 %0, %0, %4;\n\taddc.u32 c0, 0, 0;\n\t"
+        "add.cc.u32 %1, %1, %5;\n\taddc.u32 c1, 0, 0;\n\t"
+        "add.cc.u32 %2, %2, %6;\n\taddc.u32 c2, 0, 0;\n\t"
+        "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
+        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 add.u32 %3, %3, %9;\n\t}"
+        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a)
+        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "r"(dz));
 }
 
 // A frame's constants (k_tile_desc writes one per frame), staged in shared memory with each
@@ -109,7 +137,7 @@ __device__ __forceinline__ void push_work(const TilesArgs& ta, int f, int row, i
     ta.work[slot] = work_entry(f, row, cc, 0xffffu);
 }
 
-template <int NCH, int NW>
+template <int NCH, int NW, bool kZ1>
 __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc* __restrict__ out) {
     constexpr int TROWS = 32 * NW, TCOLS = 16 * NCH;
     constexpr int kShape = (NCH == 2) + 2 * (NW == 2);
@@ -124,7 +152,9 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
     const int nr1 = min(TROWS, ta.h - r0t) - 1;
     TileDesc d;
     int lo[3], hi[3];
-    bool ok = fp.plane_ok && ((fp.lin_fit >> kShape) & 1);
+    // (a frame the launch's walk variant does not fit -- only possible in a frame graph captured
+    // for another frame -- takes the exact pass tile by tile)
+    bool ok = fp.plane_ok && ((fp.lin_fit >> kShape) & 1) && (!kZ1 || (fp.lin_fit & 16));
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const long long dc = fp.Dc[k], dr = fp.Dr[k];
@@ -136,7 +166,7 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
         ok = ok && (unsigned long long)(dc < 0 ? -dc : dc) < (1ull << 32);
     }
     const int X = hi[0] - lo[0] + 1, Y = hi[1] - lo[1] + 1;
-    ok = ok && X <= kTabMaxX && Y <= kTabMaxY;
+    ok = ok && X <= kTabMaxX && Y <= TabGeom<NW>::kMaxY;
     const bool tin = lo[0] >= 0 && hi[0] <= g.nx - 1 && lo[1] >= 0 && hi[1] <= g.ny - 1 &&
                      lo[2] >= g.zb && hi[2] <= g.zb + g.nzl - 1;
     d.X0 = lo[0];
@@ -181,6 +211,7 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
 // The index taken is the one the carries of W track: when lo + te2 wraps (the pixel sits in the
 // upper half of the tie window) the index is already one step further, so later pixels' indices
 // stay exact no matter where the row starts (the pixel itself is a tie and gets deferred).
+template <int kBit = 16384>
 __device__ __forceinline__ void walk_state(long long u0, long long u1, long long u2, const TileFrame& fr,
                                            int X0, int Y0, uint32_t tab, uint32_t& w0, uint32_t& w1,
                                            uint32_t& w2, uint32_t& a) {
@@ -193,7 +224,7 @@ __device__ __forceinline__ void walk_state(long long u0, long long u1, long long
     const int ix = (int)(u0 >> 32) + (w0 < te2 ? (fr.neg[0] ? -1 : 1) : 0);
     const int iy = (int)(u1 >> 32) + (w1 < te2 ? (fr.neg[1] ? -1 : 1) : 0);
     const int iz = (int)(u2 >> 32) + (w2 < te2 ? 1 : 0);  // (only the parity matters)
-    a = tab + 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + ((uint32_t)(iz & 1) << 14);
+    a = tab + 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + ((uint32_t)(iz & 1) * (uint32_t)kBit);
 }
 
 // 32-byte row segment load (one LDG.256, L1 no-allocate: every byte is read once)
@@ -212,10 +243,19 @@ __device__ __forceinline__ void red_word(unsigned long long addr, uint32_t v) {
         "mov.b64 w, {lo, hi};\n\tred.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v) : "memory");
 }
 
-template <int NCH, int NW, bool kBox>
+// the same, predicated on v != 0 inside the asm (no branch around the RED)
+__device__ __forceinline__ void red_word_nz(unsigned long long addr, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 hi, lo;\n\t.reg .b64 w;\n\t"
+        "setp.ne.u32 p, %1, 0;\n\tshr.u32 hi, %1, 20;\n\tand.b32 lo, %1, 1048575;\n\t"
+        "mov.b64 w, {lo, hi};\n\t@p red.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v) : "memory");
+}
+
+template <int NCH, int NW, bool kBox, bool kZ1>
 __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB) k_pnn_tiles(const TilesArgs ta) {
     constexpr int NT = 32 * NW, TROWS = 32 * NW, TCOLS = 16 * NCH;
-    __shared__ __align__(16) uint32_t s_tab[kTabWords];
+    using TG = TabGeom<NW>;
+    __shared__ __align__(16) uint32_t s_tab[TG::kWords];
     __shared__ TileFrame s_frs[3];       // ring (tiles i, i + 1, i + 2): frame constants
     __shared__ TileDesc s_desc[3];       //   and descriptors, cp.async-staged
     __shared__ unsigned int s_cnt[2];    // chunks counted out of bounds / deferred (rare)
@@ -223,11 +263,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 2) s_cnt[tid] = 0u;
     if (tid == 0) s_px = 0ull;
-    for (int i = tid; i < kTabWords / 4; i += NT)
+    for (int i = tid; i < TG::kWords / 4; i += NT)
         reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0u, 0u, 0u, 0u);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(s_tab);
     // (the XOR parity needs plane 0 below 16 KB - 8 KB; otherwise every tile takes the exact pass)
-    const bool tab_ok = tab + 4u * 2048u <= 16384u;
+    const bool tab_ok = tab + 4u * (uint32_t)(TG::kMaxY * kTabStr) <= (uint32_t)TG::kBit;
     const GridDev& g = ta.g;
     const int tpf = ta.ntx * ta.nty;
     // tiles round-robin over the CTAs: the CTAs in flight together work on a window of ~grid
@@ -384,7 +424,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             uint32_t w0, w1, w2, a;
             {
                 const long long u0 = chunk_u(0, 0), u1 = chunk_u(0, 1), u2 = chunk_u(0, 2);
-                walk_state(u0, u1, u2, s_fr, X0, Y0, tab, w0, w1, w2, a);
+                walk_state<TG::kBit>(u0, u1, u2, s_fr, X0, Y0, tab, w0, w1, w2, a);
 #if SVR_TILES_PREFETCH
                 if (tin) {  // L2 prefetch of the row's first voxel line: the flush's REDs then hit L2
                     const int ix = (int)(u0 >> 32), iy = (int)(u1 >> 32), iz = (int)(u2 >> 32);
@@ -394,25 +434,37 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             }
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                if (c > 0) tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
+                if (c > 0) tile_step<TG::kBit>(w0, w1, w2, a, e0, e1, e2, sx, sy);
                 const uint32_t o20 = (wmask >> c) & 1u ? 0x00100000u : 0u;
                 uint32_t tmin = min(w0, min(w1, w2));
                 red_shared(a, __byte_perm(wd[c][0], o20, 0x7640));
+                if (kZ1) {
+                    // at most one z carry in the chunk: the z move is the fixed step to the other
+                    // parity plane (an add on the FMA pipe instead of an ALU XOR)
+                    const uint32_t dz = (a & (uint32_t)TG::kBit) ? 0u - (uint32_t)TG::kBit : (uint32_t)TG::kBit;
 #pragma unroll
-                for (int j = 1; j < kChunk; ++j) {
-                    tile_step(w0, w1, w2, a, e0, e1, e2, sx, sy);
-                    tmin = min(tmin, min(w0, min(w1, w2)));
-                    red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                    for (int j = 1; j < kChunk; ++j) {
+                        tile_step_dz(w0, w1, w2, a, e0, e1, e2, sx, sy, dz);
+                        tmin = min(tmin, min(w0, min(w1, w2)));
+                        red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 1; j < kChunk; ++j) {
+                        tile_step<TG::kBit>(w0, w1, w2, a, e0, e1, e2, sx, sy);
+                        tmin = min(tmin, min(w0, min(w1, w2)));
+                        red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                    }
                 }
                 const bool tie = o20 != 0u && tmin < tie2;
                 if (__any_sync(0xffffffffu, tie)) {  // rare: undo the chunk, send it to the exact pass
                     if (tie) {
                         uint32_t v0, v1, v2, ua;  // state at the chunk's pixel 0 (= the walk's)
-                        walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, v0, v1, v2, ua);
+                        walk_state<TG::kBit>(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, v0, v1, v2, ua);
                         red_shared(ua, 0u - __byte_perm(wd[c][0], o20, 0x7640));
 #pragma unroll
                         for (int j = 1; j < kChunk; ++j) {  // (unrolled: wd stays in registers)
-                            tile_step(v0, v1, v2, ua, e0, e1, e2, sx, sy);
+                            tile_step<TG::kBit>(v0, v1, v2, ua, e0, e1, e2, sx, sy);
                             red_shared(ua, 0u - __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
                         }
                         push_work(ta, f, row, (c0t >> 4) + c);
@@ -446,42 +498,36 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         }
         __syncthreads();  // table complete
         if (tok) {
-            // flush + zero: positions p = x + X y spread over all threads, walked incrementally
+            // flush + zero: thread (x, yr) = (tid mod X, tid div X) takes column x of the table
+            // rows yr, yr + R, ... (R = NT div X rows per pass; fixed per thread, so no wrap logic)
             const float p1 = s_fr.p1, p2 = s_fr.p2;
             const uint32_t sxy8 = (uint32_t)((long long)g.nx * g.ny * 8), nx8 = (uint32_t)g.nx * 8u;
-            const int XY = X * Y;
             const float rX = 1.0f / (float)X;
-            // y = p / X exactly: the quotients' fractional parts are >= 1/(2X) from an integer
-            const int y0 = (int)(((float)tid + 0.5f) * rX);
-            int x = tid - y0 * X;
-            const int dy = (int)(((float)NT + 0.5f) * rX), dx = NT - dy * X;
-            int ti = x + kTabStr * y0;
-            uint32_t go = (uint32_t)y0 * nx8 + (uint32_t)x * 8u;
-            float tt = fmaf(p2, (float)y0, fmaf(p1, (float)x, tt0));
-            const int dti = dx + kTabStr * dy, wti = kTabStr - X;
-            const uint32_t dgo = (uint32_t)dy * nx8 + (uint32_t)dx * 8u, wgo = nx8 - 8u * (uint32_t)X;
-            const float dtt = p1 * (float)dx + p2 * (float)dy, wtt = p2 - p1 * (float)X;
-            for (int p = tid; p < XY; p += NT) {
-                const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + kTabPlane];
-                s_tab[ti] = 0u;
-                s_tab[ti + kTabPlane] = 0u;
-                const uint32_t k = (uint32_t)(int)ceilf(tt);  // k - kmin >= 0
-                const bool odd = ((k ^ zpar) & 1u) != 0u;
-                const unsigned long long a0 = fbase + (k * sxy8 + go);
-                // per slot: an empty slot's voxel may lie outside the slab (face tiles), and a
-                // RED of 0 would still pull its line into L2 and write it back
-                const uint32_t vlo = odd ? v1 : v0, vhi = odd ? v0 : v1;
-                if (vlo) red_word(a0, vlo);
-                if (vhi) red_word(a0 + sxy8, vhi);
-                x += dx;
-                ti += dti;
-                go += dgo;
-                tt += dtt;
-                if (x >= X) {
-                    x -= X;
-                    ti += wti;
-                    go += wgo;
-                    tt += wtt;
+            // exact quotients: (a + 1/2) / X is >= 1/(2X) from an integer for X <= 32
+            const int yr = (int)(((float)tid + 0.5f) * rX), R = (int)(((float)NT + 0.5f) * rX);
+            const int x = tid - yr * X;
+            if (yr < R) {
+                int ti = x + kTabStr * yr;
+                uint32_t go = (uint32_t)yr * nx8 + (uint32_t)x * 8u;
+                const float ttx = fmaf(p1, (float)x, tt0), Rf = (float)R;
+                float yf = (float)yr;
+                const int dti = kTabStr * R;
+                const uint32_t dgo = (uint32_t)R * nx8;
+                for (int y = yr; y < Y; y += R) {
+                    const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + TG::kPlane];
+                    s_tab[ti] = 0u;
+                    s_tab[ti + TG::kPlane] = 0u;
+                    const uint32_t k = (uint32_t)(int)ceilf(fmaf(p2, yf, ttx));  // k - kmin >= 0
+                    const bool odd = ((k ^ zpar) & 1u) != 0u;
+                    const unsigned long long a0 = fbase + (k * sxy8 + go);
+                    // per slot: an empty slot's voxel may lie outside the slab (face tiles), and a
+                    // RED of 0 would still pull its line into L2 and write it back
+                    const uint32_t vlo = odd ? v1 : v0, vhi = odd ? v0 : v1;
+                    red_word_nz(a0, vlo);
+                    red_word_nz(a0 + sxy8, vhi);
+                    ti += dti;
+                    go += dgo;
+                    yf += Rf;
                 }
             }
         }
