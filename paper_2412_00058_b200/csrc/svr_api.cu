@@ -288,6 +288,7 @@ struct PrepCtx {
 // A launch's shape carries bit 2 (kShapeZ1) when every frame has at most one z carry per chunk
 // (FrameParams::lin_fit bit 4): the kZ1 walk variant.
 constexpr int kShapeZ1 = 4, kFitZ1 = 16;
+
 static inline int shape_cols(int s) { return (s & 1) ? 32 : 64; }
 static inline int shape_rows(int s) { return (s & 2) ? 64 : 128; }
 
@@ -304,9 +305,7 @@ static int tile_shapes_fit(const long long Dc[3], const long long Dr[3], int cou
         const double c1 = shape_cols(sh) - 1, r1 = shape_rows(sh) - 1;
         const double spx = (c1 * std::fabs((double)Dc[0]) + r1 * std::fabs((double)Dr[0])) * s;
         const double spy = (c1 * std::fabs((double)Dc[1]) + r1 * std::fabs((double)Dr[1])) * s;
-        // (table rows: 62 for 128-row tiles, 31 for 64-row ones: TabGeom in svr_k1.cuh)
-        const double ymax = shape_rows(sh) == 128 ? 62 : 31;
-        if (std::floor(spx + 1e-9) + 2 <= 32 && std::floor(spy + 1e-9) + 2 <= ymax) m |= 1 << sh;
+        if (std::floor(spx + 1e-9) + 2 <= 32 && std::floor(spy + 1e-9) + 2 <= 62) m |= 1 << sh;
     }
     return m;
 }

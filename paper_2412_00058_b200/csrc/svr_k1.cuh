@@ -47,14 +47,13 @@ constexpr int kTabMaxY = 62;                   // voxel rows (62 * 33 <= 2048 wo
 constexpr int kTabMaxX = 32;                   // voxel columns
 constexpr int kTabWords = kTabPlane + 2048;    // 24 KB (the 8 KB gap is unused)
 
-// k_pnn_tiles table geometry per tile height: 128-row tiles (NW = 4) as above; 64-row tiles
-// (NW = 2) need at most 31 voxel rows, so plane 1 sits 8 KB up (bit 13) and the table is 12 KB --
-// small enough for 14 two-warp CTAs per SM (the same 28 warps, barriers over 2 warps instead of 4)
+// k_pnn_tiles table geometry (one for every tile height: a 12 KB table of 31 rows for the 64-row
+// tiles measured no faster and refused frames with long row steps)
 template <int NW>
 struct TabGeom {
-    static constexpr int kBit = NW == 4 ? 16384 : 8192;  // byte distance of the parity planes
-    static constexpr int kPlane = kBit / 4;               // in words
-    static constexpr int kMaxY = NW == 4 ? 62 : 31;
+    static constexpr int kBit = 16384;       // byte distance of the parity planes
+    static constexpr int kPlane = kBit / 4;  // in words
+    static constexpr int kMaxY = kTabMaxY;
     static constexpr int kWords = kPlane + ((kMaxY * kTabStr + 3) & ~3);
 };
 
@@ -211,10 +210,9 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
 // The index taken is the one the carries of W track: when lo + te2 wraps (the pixel sits in the
 // upper half of the tie window) the index is already one step further, so later pixels' indices
 // stay exact no matter where the row starts (the pixel itself is a tie and gets deferred).
-template <int kBit = 16384>
 __device__ __forceinline__ void walk_state(long long u0, long long u1, long long u2, const TileFrame& fr,
-                                           int X0, int Y0, uint32_t tab, uint32_t& w0, uint32_t& w1,
-                                           uint32_t& w2, uint32_t& a) {
+                                           int X0, int Y0, uint32_t tab, uint32_t pb, uint32_t& w0,
+                                           uint32_t& w1, uint32_t& w2, uint32_t& a) {
     const uint32_t te2 = fr.te2;
     const uint32_t m0 = (uint32_t)u0 ^ fr.neg[0], m1 = (uint32_t)u1 ^ fr.neg[1], m2 = (uint32_t)u2 ^ fr.neg[2];
     w0 = m0 + te2;
@@ -224,7 +222,7 @@ __device__ __forceinline__ void walk_state(long long u0, long long u1, long long
     const int ix = (int)(u0 >> 32) + (w0 < te2 ? (fr.neg[0] ? -1 : 1) : 0);
     const int iy = (int)(u1 >> 32) + (w1 < te2 ? (fr.neg[1] ? -1 : 1) : 0);
     const int iz = (int)(u2 >> 32) + (w2 < te2 ? 1 : 0);  // (only the parity matters)
-    a = tab + 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + ((uint32_t)(iz & 1) * (uint32_t)kBit);
+    a = tab + 4u * (uint32_t)((ix - X0) + kTabStr * (iy - Y0)) + (uint32_t)(iz & 1) * pb;  // pb: plane bytes
 }
 
 // 32-byte row segment load (one LDG.256, L1 no-allocate: every byte is read once)
@@ -424,7 +422,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             uint32_t w0, w1, w2, a;
             {
                 const long long u0 = chunk_u(0, 0), u1 = chunk_u(0, 1), u2 = chunk_u(0, 2);
-                walk_state<TG::kBit>(u0, u1, u2, s_fr, X0, Y0, tab, w0, w1, w2, a);
+                walk_state(u0, u1, u2, s_fr, X0, Y0, tab, (uint32_t)TG::kBit, w0, w1, w2, a);
 #if SVR_TILES_PREFETCH
                 if (tin) {  // L2 prefetch of the row's first voxel line: the flush's REDs then hit L2
                     const int ix = (int)(u0 >> 32), iy = (int)(u1 >> 32), iz = (int)(u2 >> 32);
@@ -460,7 +458,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 if (__any_sync(0xffffffffu, tie)) {  // rare: undo the chunk, send it to the exact pass
                     if (tie) {
                         uint32_t v0, v1, v2, ua;  // state at the chunk's pixel 0 (= the walk's)
-                        walk_state<TG::kBit>(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, v0, v1, v2, ua);
+                        walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, (uint32_t)TG::kBit, v0, v1, v2, ua);
                         red_shared(ua, 0u - __byte_perm(wd[c][0], o20, 0x7640));
 #pragma unroll
                         for (int j = 1; j < kChunk; ++j) {  // (unrolled: wd stays in registers)
