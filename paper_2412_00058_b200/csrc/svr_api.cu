@@ -285,8 +285,8 @@ struct PrepCtx {
 };
 
 // k_pnn_tiles shapes (svr_k1.cuh): s = (NCH == 2) + 2 (NW == 2); columns 16 NCH x rows 32 NW.
-// A launch's shape carries bit 2 (kShapeZ1) when every frame has at most one z carry per chunk
-// (FrameParams::lin_fit bit 4): the kZ1 walk variant.
+// A launch's shape carries bit 2 (kShapeZ1) when every frame has at most one y and one z carry
+// per chunk (FrameParams::lin_fit bit 4): the kZ1 walk variant.
 constexpr int kShapeZ1 = 4, kFitZ1 = 16;
 
 static inline int shape_cols(int s) { return (s & 1) ? 32 : 64; }
@@ -425,8 +425,9 @@ static int make_params(const svr_rigid& pose, const PrepCtx& x, double sx, doubl
         const double qp2 = pose.qw * pose.qw + pose.qx * pose.qx + pose.qy * pose.qy + pose.qz * pose.qz;
         if (fp->plane_ok && x.lin_ok && qp2 >= 0.98)  // (the count bound in prep_ctx assumes |q|^2 >= 0.98)
             fp->lin_fit = tile_shapes_fit(fp->Dc, fp->Dr, x.lin_count_ok);
-        // kZ1 walk: at most one z carry in the 15 steps of a 16-pixel chunk
-        if (fp->lin_fit && 15 * std::llabs(fp->Dc[2]) < (1ll << 32)) fp->lin_fit |= kFitZ1;
+        // kZ1 walk: at most one y and one z carry in the 15 steps of a 16-pixel chunk
+        if (fp->lin_fit && 15 * std::llabs(fp->Dc[1]) < (1ll << 32) && 15 * std::llabs(fp->Dc[2]) < (1ll << 32))
+            fp->lin_fit |= kFitZ1;
     }
     return SVR_OK;
 }

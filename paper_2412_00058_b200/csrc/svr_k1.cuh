@@ -14,17 +14,20 @@
 // on B200: tools/ubench_atoms.cu; the bank model is in profiles/r2_opt_log.md).
 //
 // Per pixel the walk is, in SASS, 3 x (IADD3 with carry-out to a predicate + one predicated
-// address update) + a 3-input min (tie screen) + PRMT + ATOMS: the fixed-point fractions of
+// address update) + the tie screen + PRMT + ATOMS: the fixed-point fractions of
 // u = K + col*Dc + row*Dr (32.32) are stepped exactly, the index moves where a
 // fraction carries, and the shared-table byte address moves with it (x: +-4, y: +-4*STR,
-// z: XOR of the parity plane bit 1 << 13; a B-scan plane puts <= 2 z values in a voxel column).
+// z: to the other parity plane, bit 1 << 14; a B-scan plane puts <= 2 z values in a voxel column).
+// The kZ1 variant (frames with at most one y and one z carry per 16-pixel chunk) keeps the ALU
+// pipe, the walk's limit, to the carries, an x-only tie screen and the PRMT: the z move is a
+// predicated add and the y / z post-carry fractions are captured by predicated FMA-pipe moves.
 // A 16-pixel chunk whose fractions came within the certified tie window is undone and its
 // pixels go to the exact worklist pass (k_pnn_work), as before.
 //
-// Flush: the table's X x Y positions are spread linearly over all threads; each reads and
-// zeroes both parity slots (so the next tile starts from a clean table without a separate
-// zeroing pass), finds the slots' z from the frame plane and issues one predicated 64-bit
-// red.global.add per non-empty slot.
+// Flush: thread (x, r) reads and zeroes both parity slots of table column x in rows r, r + R, ...
+// (R = threads div X; the next tile then starts from a clean table without a zeroing pass), finds
+// the slots' z from the frame plane and issues one predicated 64-bit red.global.add per non-empty
+// slot.
 #pragma once
 
 #ifndef SVR_TILES_PREFETCH
@@ -103,20 +106,25 @@ __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& 
         : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "n"(kBit));
 }
 
-// tile_step for chunks with at most one z carry (kZ1): the z move is +-16 KB (dz, fixed per chunk
-// by its start parity) as a predicated add, which ptxas puts on the FMA pipe like the x and y
-// moves -- the walk is ALU-bound (carries, tie screen, PRMT), the FMA pipe had room
-__device__ __forceinline__ void tile_step_dz(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
-                                             uint32_t e0, uint32_t e1, uint32_t e2, uint32_t sx,
-                                             uint32_t sy, uint32_t dz) {
+// kZ1 step (at most one y and one z carry per chunk, tile_shapes_fit): the z move is +-16 KB
+// (dz, fixed per chunk by its start parity) as a predicated add, which ptxas puts on the FMA pipe
+// like the x and y moves -- the walk is ALU-bound (carries, tie screen, PRMT); where y or z carries
+// its new (post-carry) fraction is captured into ty / tz with a predicated multiply by an opaque
+// 1 (an FMA-pipe move; a tie in y or z can only sit at the chunk start or right after its one
+// carry), so the per-pixel tie screen needs only x on the ALU pipe
+__device__ __forceinline__ void tile_step_cap(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
+                                              uint32_t& ty, uint32_t& tz, uint32_t e0, uint32_t e1,
+                                              uint32_t e2, uint32_t sx, uint32_t sy, uint32_t dz,
+                                              uint32_t one) {
     asm("{\n\t.reg .pred p0, p1, p2;\n\t.reg .u32 c0, c1, c2;\n\t"
-        "add.cc.u32 %0, %0, %4;\n\taddc.u32 c0, 0, 0;\n\t"
-        "add.cc.u32 %1, %1, %5;\n\taddc.u32 c1, 0, 0;\n\t"
-        "add.cc.u32 %2, %2, %6;\n\taddc.u32 c2, 0, 0;\n\t"
+        "add.cc.u32 %0, %0, %6;\n\taddc.u32 c0, 0, 0;\n\t"
+        "add.cc.u32 %1, %1, %7;\n\taddc.u32 c1, 0, 0;\n\t"
+        "add.cc.u32 %2, %2, %8;\n\taddc.u32 c2, 0, 0;\n\t"
         "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
-        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 add.u32 %3, %3, %9;\n\t}"
-        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a)
-        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "r"(dz));
+        "@p0 add.u32 %3, %3, %9;\n\t@p1 add.u32 %3, %3, %10;\n\t@p2 add.u32 %3, %3, %11;\n\t"
+        "@p1 mul.lo.u32 %4, %1, %12;\n\t@p2 mul.lo.u32 %5, %2, %12;\n\t}"
+        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a), "+r"(ty), "+r"(tz)
+        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "r"(dz), "r"(one));
 }
 
 // A frame's constants (k_tile_desc writes one per frame), staged in shared memory with each
@@ -126,7 +134,7 @@ struct __align__(16) TileFrame {
     uint32_t E[3], neg[3];         // |Dc| low words; all-ones when Dc < 0 (mirrored fractions)
     uint32_t te2, sx, sy;          // tie window + 1; table byte steps along x and y
     float p1, p2;                  // frame plane slopes (FrameParams::pz[1], pz[2])
-    uint32_t pad;
+    uint32_t pad;                  // 1
 };
 static_assert(sizeof(TileFrame) == 96, "TileFrame is staged as 6 x 16 bytes");
 
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
         fr.sy = fp.Dc[1] < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
         fr.p1 = (float)fp.pz[1];
         fr.p2 = (float)fp.pz[2];
-        fr.pad = 0u;
+        fr.pad = 1u;  // (an opaque 1: tile_step_cap's predicated moves)
         ta.frc[f] = fr;
     }
 }
@@ -418,6 +426,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         if (tok && warp < S) {
             const uint32_t e0 = s_fr.E[0], e1 = s_fr.E[1], e2 = s_fr.E[2], sx = s_fr.sx, sy = s_fr.sy;
             const uint32_t tie2 = 2u * s_fr.te2;
+            const uint32_t one = s_fr.pad;  // (kZ1: tile_step_cap's opaque 1)
             // walk state at pixel 0 of the row
             uint32_t w0, w1, w2, a;
             {
@@ -437,15 +446,19 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 uint32_t tmin = min(w0, min(w1, w2));
                 red_shared(a, __byte_perm(wd[c][0], o20, 0x7640));
                 if (kZ1) {
-                    // at most one z carry in the chunk: the z move is the fixed step to the other
-                    // parity plane (an add on the FMA pipe instead of an ALU XOR)
+                    // at most one y and one z carry in the chunk: the z move is the fixed step to
+                    // the other parity plane (an add on the FMA pipe instead of an ALU XOR)
                     const uint32_t dz = (a & (uint32_t)TG::kBit) ? 0u - (uint32_t)TG::kBit : (uint32_t)TG::kBit;
+                    // y and z ties can only sit at the chunk start (screened above) or right after
+                    // their one carry: those fractions are captured, so per pixel only x is screened
+                    uint32_t ty = 0xffffffffu, tz = 0xffffffffu;
 #pragma unroll
                     for (int j = 1; j < kChunk; ++j) {
-                        tile_step_dz(w0, w1, w2, a, e0, e1, e2, sx, sy, dz);
-                        tmin = min(tmin, min(w0, min(w1, w2)));
+                        tile_step_cap(w0, w1, w2, a, ty, tz, e0, e1, e2, sx, sy, dz, one);
+                        tmin = min(tmin, w0);
                         red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
                     }
+                    tmin = min(tmin, min(ty, tz));
                 } else {
 #pragma unroll
                     for (int j = 1; j < kChunk; ++j) {
