@@ -1,2 +1,2 @@
-SVR_LIB_PATH=$PWD/abtmp/tiecap.so timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
-bash tools/_ab.sh
+timeout 900 python -m pytest tests -m gpu -x -q -k "tri or cfg5" > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
+bash tools/_ab_cfg.sh cfg5
