@@ -292,10 +292,19 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
     BoxAcc bb;
     const uint32_t sxy8 = (uint32_t)((long long)g.nx * g.ny * 8), nx8 = (uint32_t)g.nx * 8u;
 
+    // this thread's 32 samples, one 16-sample chunk per wd[c]; the next tile's chunk c is requested
+    // as soon as the current tile's chunk c has been walked (its registers are free), so a direct
+    // tile -- no flush to hide the load behind -- finds its samples mostly arrived
     uint32_t wd[NCH][4];
     auto load_px = [&](int fq, int tyq, int txq) {
         const int line = min(tyq * kFanLines + lane, fa.h - 1);
         ld256(fa.px + (long long)fq * fa.fstride + (long long)line * fa.pitch + txq * TCOLS + 32 * warp, &wd[0][0]);
+    };
+    auto load_half = [&](int c, int fq, int tyq, int txq) {
+        const int line = min(tyq * kFanLines + lane, fa.h - 1);
+        const uint8_t* p = fa.px + (long long)fq * fa.fstride + (long long)line * fa.pitch + txq * TCOLS + 32 * warp + 16 * c;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(wd[c][0]), "=r"(wd[c][1]), "=r"(wd[c][2]), "=r"(wd[c][3]) : "l"(p));
     };
     // threads 0..95 stage a tile's 32 scanline constants (1.5 KB), 96..99 its descriptor
     auto stage = [&](int fq, int tyq, int txq, int b) {
@@ -349,6 +358,7 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
         if (t + 2 * tstep < t1) stage(f2, ty2, tx2, b == 0 ? 2 : b - 1);
         commit();
         const FanDesc& dsc = s_desc[b];
+        const bool more = t + tstep < t1;  // (a next tile exists: its samples are requested below)
         const int nlines = min(kFanLines, fa.h - ty * kFanLines);
         const int line = ty * kFanLines + lane;
         const bool act = lane < nlines;
@@ -417,6 +427,7 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
                     } else if (kBox && o20 != 0u) {
                         fan_box(bb, A, D, cth + 16 * c, 16);
                     }
+                    if (more) load_half(c, fn, tyn, txn);
                 }
             } else {
                 const uint32_t sx = neg[0] ? 0u - 8u : 8u, sy = neg[1] ? 0u - nx8 : nx8, sz = neg[2] ? 0u - sxy8 : sxy8;
@@ -433,6 +444,7 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
                         tmin = min(tmin, min(v0, min(v1, v2)));
                         run += __byte_perm(wd[c][j >> 2], 0x00100000u, 0x7640 | (j & 3));
                     }
+                    if (more) load_half(c, fn, tyn, txn);
                     const bool in = (wmask >> c) & 1u, keep = in && tmin >= tie2;
                     if (in && !keep) {  // rare: the chunk's runs are dropped, it goes to the exact pass
                         push_fan(fa, f, line, (cth >> 4) + c);
@@ -449,11 +461,13 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
                 }
             }
         }
+        else if (more) {
+            load_px(fn, tyn, txn);
+        }
         if (noob) atomicAdd(&s_cnt[0], noob);
         if (ndef) atomicAdd(&s_cnt[1], ndef);
         if (tid == 0) s_px += (unsigned long long)TCOLS * (unsigned long long)nlines;
-        wait_stage();  // (before the pixel load: the wait would also cover it)
-        if (t + tstep < t1) load_px(fn, tyn, txn);
+        wait_stage();
         if (table) {  // (CTA-uniform)
             __syncthreads();  // table complete
             const int X = dsc.XY & 0xffff, Y = dsc.XY >> 16, stride = dsc.stride;

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "tri or cfg5" > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
-bash tools/_ab_cfg.sh cfg5
+timeout 900 python -m pytest tests -m gpu -x -q -k "fan or cfg3 or fullsize or parity" > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
+bash tools/_ab_cfg.sh cfg3
