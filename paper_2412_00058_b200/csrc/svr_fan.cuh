@@ -186,6 +186,28 @@ __device__ __forceinline__ void off_step(uint32_t& w0, uint32_t& w1, uint32_t& w
         : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "r"(sz));
 }
 
+// tile_step with the z toggle kept in its own register (the table address is a ^ zo): the shared
+// atomic's address is then a fresh register, so the next sample's in-place x / y moves do not wait
+// for the atomic to read it (a write-after-read stall: short_sb at every move after an ATOMS)
+__device__ __forceinline__ void tile_step_zx(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a, uint32_t& zo,
+                                             uint32_t e0, uint32_t e1, uint32_t e2, uint32_t sx, uint32_t sy) {
+    asm("{\n\t.reg .pred p0, p1, p2;\n\t.reg .u32 c0, c1, c2;\n\t"
+        "add.cc.u32 %0, %0, %5;\n\taddc.u32 c0, 0, 0;\n\t"
+        "add.cc.u32 %1, %1, %6;\n\taddc.u32 c1, 0, 0;\n\t"
+        "add.cc.u32 %2, %2, %7;\n\taddc.u32 c2, 0, 0;\n\t"
+        "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
+        "@p0 add.u32 %3, %3, %8;\n\t@p1 add.u32 %3, %3, %9;\n\t@p2 xor.b32 %4, %4, 16384;\n\t}"
+        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a), "+r"(zo)
+        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy));
+}
+
+#ifndef SVR_FAN_ZX
+#define SVR_FAN_ZX 1  // k_fan_tiles table walk: z toggle in its own register (tile_step_zx)
+#endif
+#ifndef SVR_FAN_DRAINPF
+#define SVR_FAN_DRAINPF 1  // k_fan_tiles: the run buffer's next entry read while the current one is added
+#endif
+
 // Chunk classes of one thread's 32-sample segment (k_pnn_tiles' rule): a chunk whose index range
 // lies inside the grid / slab is walked, one wholly outside is counted out of bounds, one
 // straddling a face goes to the exact pass.  Returns the mask of chunks to walk.
@@ -401,6 +423,7 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
                 const uint32_t sx = neg[0] ? 0u - 4u : 4u;
                 const uint32_t sy = neg[1] ? 0u - 4u * (uint32_t)stride : 4u * (uint32_t)stride;
                 uint32_t a = tab + 4u * (uint32_t)((ix - dsc.X0) + stride * (iy - dsc.Y0)) + ((uint32_t)(iz & 1) << 14);
+                uint32_t zo = 0u;
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
                     if (c > 0) tile_step(v0, v1, v2, a, e[0], e[1], e[2], sx, sy);
@@ -410,10 +433,18 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
                     red_shared(a, __byte_perm(wd[c][0], o20, 0x7640));
 #pragma unroll
                     for (int j = 1; j < kChunk; ++j) {
+#if SVR_FAN_ZX
+                        tile_step_zx(v0, v1, v2, a, zo, e[0], e[1], e[2], sx, sy);
+                        tmin = min(tmin, min(v0, min(v1, v2)));
+                        red_shared(a ^ zo, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+#else
                         tile_step(v0, v1, v2, a, e[0], e[1], e[2], sx, sy);
                         tmin = min(tmin, min(v0, min(v1, v2)));
                         red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+#endif
                     }
+                    a ^= zo;
+                    zo = 0u;
                     if (o20 != 0u && tmin < tie2) {  // rare: undo the chunk, send it to the exact pass
                         uint32_t r0 = q0, r1 = q1, r2 = q2, ra = ua;
                         red_shared(ra, 0u - __byte_perm(wd[c][0], o20, 0x7640));
@@ -451,12 +482,30 @@ __global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs
                         ++ndef;
                     }
                     if (keep) red_word(gb + off, run);  // the open run
+#if SVR_FAN_DRAINPF
+                    // software-pipelined: entry k + 1 is read (and zeroed) before entry k's RED
+                    if (rbuf != ptr) {
+                        uint32_t o, r, q = rbuf;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n\tst.shared.v2.u32 [%2], {%3, %3};"
+                                     : "=r"(o), "=r"(r) : "r"(q), "r"(0u) : "memory");
+                        for (q += 8u * NT; q != ptr; q += 8u * NT) {
+                            uint32_t on, rn;
+                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n\tst.shared.v2.u32 [%2], {%3, %3};"
+                                         : "=r"(on), "=r"(rn) : "r"(q), "r"(0u) : "memory");
+                            if (keep) red_word(gb + o, r);
+                            o = on;
+                            r = rn;
+                        }
+                        if (keep) red_word(gb + o, r);
+                    }
+#else
                     for (uint32_t q = rbuf; q != ptr; q += 8u * NT) {
                         uint32_t o, r;
                         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n\tst.shared.v2.u32 [%2], {%3, %3};"
                                      : "=r"(o), "=r"(r) : "r"(q), "r"(0u) : "memory");
                         if (keep) red_word(gb + o, r);
                     }
+#endif
                     if (kBox && keep) fan_box(bb, A, D, cth + 16 * c, 16);
                 }
             }
