@@ -288,6 +288,9 @@ struct PrepCtx {
 // A launch's shape carries bit 2 (kShapeZ1) when every frame has at most one y and one z carry
 // per chunk (FrameParams::lin_fit bit 4): the kZ1 walk variant.
 constexpr int kShapeZ1 = 4, kFitZ1 = 16;
+#ifndef SVR_FILL_TY
+#define SVR_FILL_TY 8  // batch fill: rows per warp of k_fill_warp
+#endif
 
 static inline int shape_cols(int s) { return (s & 1) ? 32 : 64; }
 static inline int shape_rows(int s) { return (s & 2) ? 64 : 128; }
@@ -1484,8 +1487,8 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
             for (const Box& b : bs) {
                 BoxTiles t;
                 t.b = b;
-                t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of 8 rows
-                t.nty = (b.y1 - b.y0 + 1 + 31) / 32;
+                t.ntx = (b.x1 - b.x0 + 1 + 29) / 30;  // k_fill_warp: 30 columns x 4 warps of TY rows
+                t.nty = (b.y1 - b.y0 + 1 + 4 * SVR_FILL_TY - 1) / (4 * SVR_FILL_TY);
                 t.first = total;
                 total += (long long)t.ntx * t.nty * ((b.z1 - b.z0 + 1 + zc - 1) / zc);
                 bt.push_back(t);
@@ -1505,7 +1508,7 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         const dim3 grd = grid_1d(total);
         const BoxTiles* dt = (const BoxTiles*)d;
         const int nb = (int)bt.size();
-#define FW(Z, C) k_fill_warp<Z, 1, 8, C><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, C ? v->d_counter : nullptr)
+#define FW(Z, C) k_fill_warp<Z, 1, SVR_FILL_TY, C><<<grd, 128, 0, v->stream>>>(v->acc, v->fill, g, dt, nb, C ? v->d_counter : nullptr)
         if (count) {
             if (zc == 8) FW(8, true);
             else if (zc == 16) FW(16, true);
