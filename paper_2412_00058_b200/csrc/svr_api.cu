@@ -112,7 +112,10 @@ struct svr_volume {
     // double-buffered host side: the next call fills one pinned buffer while the previous
     // call's upload from the other is still queued behind that call's kernels
     FrameParams* h_params[2] = {nullptr, nullptr};
-    FrameParams* d_params = nullptr;
+    FrameParams* d_params = nullptr;            // = d_params2[pslot] during an insert call
+    FrameParams* d_params2[2] = {nullptr, nullptr};
+    cudaStream_t param_stream = nullptr;         // the parameter upload, off the kernels' stream
+    cudaEvent_t params_used[2] = {nullptr, nullptr};  // last kernel reading d_params2[i] done
     int params_cap = 0;
     int pslot = 0;
     cudaEvent_t params_ev[2] = {nullptr, nullptr};
@@ -712,6 +715,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaSetDevice(v->device);
     if (v->stream) cudaStreamSynchronize(v->stream);
     if (v->copy_stream) cudaStreamSynchronize(v->copy_stream);
+    if (v->param_stream) cudaStreamSynchronize(v->param_stream);
     cudaFree(v->acc);
     cudaFree(v->tri);
     cudaFree(v->fill);
@@ -721,7 +725,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     cudaFree(v->r_max);
     cudaFree(v->d_stats);
     cudaFree(v->d_counter);
-    cudaFree(v->d_params);
+    for (int i = 0; i < 2; ++i) cudaFree(v->d_params2[i]);
     for (int i = 0; i < 2; ++i) cudaFreeHost(v->h_params[i]);
     cudaFree(v->d_boxes);
     cudaFreeHost(v->h_boxes);
@@ -754,11 +758,14 @@ extern "C" int svr_destroy(svr_volume* v) {
         if (v->ev_free[i]) cudaEventDestroy(v->ev_free[i]);
         if (v->ev_h2d[i]) cudaEventDestroy(v->ev_h2d[i]);
     }
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i) {
         if (v->params_ev[i]) cudaEventDestroy(v->params_ev[i]);
+        if (v->params_used[i]) cudaEventDestroy(v->params_used[i]);
+    }
     if (v->own_stream && v->stream) cudaStreamDestroy(v->stream);
     if (v->own_stream_saved) cudaStreamDestroy(v->own_stream_saved);
     if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
+    if (v->param_stream) cudaStreamDestroy(v->param_stream);
     cudaGetLastError();
     delete v;
     return SVR_OK;
@@ -786,6 +793,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     const long long ncol = (long long)desc->nx * (desc->z_end - desc->z_begin);
     cudaError_t e = cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&v->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&v->param_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) {
         if (desc->accum == SVR_ACC_PNN) {
             e = cudaMalloc(&v->acc, sizeof(ull) * v->nvox);
@@ -808,8 +816,10 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     }
     if (e == cudaSuccess) e = cudaMalloc(&v->d_stats, sizeof(ull) * kStCount);
     if (e == cudaSuccess) e = cudaMalloc(&v->d_counter, sizeof(ull) * 2);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&v->params_ev[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->params_used[i], cudaEventDisableTiming);
+    }
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&v->ev_ready[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_free[i], cudaEventDisableTiming);
@@ -897,14 +907,16 @@ static int ensure_params(svr_volume* v, int n) {
     if (n <= v->params_cap) return SVR_OK;
     int cap = std::max(n, 2 * v->params_cap);
     CK(cudaStreamSynchronize(v->stream));
-    cudaFree(v->d_params);
+    CK(cudaStreamSynchronize(v->param_stream));
     v->d_params = nullptr;
     for (int i = 0; i < 2; ++i) {
+        cudaFree(v->d_params2[i]);
+        v->d_params2[i] = nullptr;
         cudaFreeHost(v->h_params[i]);
         v->h_params[i] = nullptr;
     }
     v->params_cap = 0;
-    CK(cudaMalloc(&v->d_params, sizeof(FrameParams) * cap));
+    for (int i = 0; i < 2; ++i) CK(cudaMalloc(&v->d_params2[i], sizeof(FrameParams) * cap));
     for (int i = 0; i < 2; ++i) CK(cudaMallocHost(&v->h_params[i], sizeof(FrameParams) * cap));
     v->params_cap = cap;
     return SVR_OK;
@@ -1307,9 +1319,25 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
     // k_pnn_tiles shapes every frame of the call fits (FrameParams::lin_fit)
     v->lin_shapes_cur = 0xf | kFitZ1;
     for (int k = 0; k < n; ++k) v->lin_shapes_cur &= hp[k].lin_fit;
-    CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
-                       v->stream));
-    CK(cudaEventRecord(v->params_ev[v->pslot], v->stream));
+    // the upload runs on its own stream, so it overlaps the kernels still queued on v->stream
+    // (the previous step's fill / render) instead of sitting on their critical path: ~1 MB for
+    // a 2400-frame call, ~20 us at PCIe speed.  d_params2 is double-buffered like h_params: the
+    // copy into slot i waits for the last kernel that read it (two calls back).  (Under stream
+    // capture the upload stays in-stream: no cross-stream dependencies in a captured graph.)
+    v->d_params = v->d_params2[v->pslot];
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(v->stream, &cap_st));
+    if (cap_st == cudaStreamCaptureStatusNone) {
+        CK(cudaStreamWaitEvent(v->param_stream, v->params_used[v->pslot], 0));
+        CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
+                           v->param_stream));
+        CK(cudaEventRecord(v->params_ev[v->pslot], v->param_stream));
+        CK(cudaStreamWaitEvent(v->stream, v->params_ev[v->pslot], 0));
+    } else {
+        CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
+                           v->stream));
+        CK(cudaEventRecord(v->params_ev[v->pslot], v->stream));
+    }
     const DevCalib cal = dev_calib(*c);
     int* boxes = nullptr;
     if (want_box) {
@@ -1320,9 +1348,12 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
         CKL();
     }
     bool pinned = false;
-    if (is_device_ptr(px, &pinned))
-        return insert_device(v, mode, px, pitch, fstride, w, h, n, v->d_params, cal, skip_zero,
-                             want_box, boxes, mark, tag, stats);
+    if (is_device_ptr(px, &pinned)) {
+        const int e = insert_device(v, mode, px, pitch, fstride, w, h, n, v->d_params, cal, skip_zero,
+                                    want_box, boxes, mark, tag, stats);
+        CK(cudaEventRecord(v->params_used[v->pslot], v->stream));
+        return e;
+    }
     // host frames: double-buffered pinned staging, H2D on copy_stream overlapped with kernels
     const long long fb = (long long)w * h;                   // packed frame bytes
     const long long pfb = (fb + 31) / 32 * 32;               // 32-B aligned frame stride
@@ -1368,6 +1399,7 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
             return e;
         CK(cudaEventRecord(v->ev_free[b], v->stream));
     }
+    CK(cudaEventRecord(v->params_used[v->pslot], v->stream));
     return SVR_OK;
 }
 
