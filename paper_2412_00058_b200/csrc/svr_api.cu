@@ -116,6 +116,9 @@ struct svr_volume {
     FrameParams* d_params2[2] = {nullptr, nullptr};
     cudaStream_t param_stream = nullptr;         // the parameter upload, off the kernels' stream
     cudaEvent_t params_used[2] = {nullptr, nullptr};  // last kernel reading d_params2[i] done
+    cudaEvent_t ins_done = nullptr;   // the last insert call's kernels done (param_stream waits)
+    cudaEvent_t ev_prep = nullptr;    // param_stream's share of the current call done
+    bool prep_on_param = false;       // insert_common: K1's per-tile setup goes to param_stream
     int params_cap = 0;
     int pslot = 0;
     cudaEvent_t params_ev[2] = {nullptr, nullptr};
@@ -762,6 +765,8 @@ extern "C" int svr_destroy(svr_volume* v) {
         if (v->params_ev[i]) cudaEventDestroy(v->params_ev[i]);
         if (v->params_used[i]) cudaEventDestroy(v->params_used[i]);
     }
+    if (v->ins_done) cudaEventDestroy(v->ins_done);
+    if (v->ev_prep) cudaEventDestroy(v->ev_prep);
     if (v->own_stream && v->stream) cudaStreamDestroy(v->stream);
     if (v->own_stream_saved) cudaStreamDestroy(v->own_stream_saved);
     if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
@@ -820,6 +825,8 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
         e = cudaEventCreateWithFlags(&v->params_ev[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->params_used[i], cudaEventDisableTiming);
     }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ins_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_prep, cudaEventDisableTiming);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&v->ev_ready[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_free[i], cudaEventDisableTiming);
@@ -1108,7 +1115,15 @@ static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
         v->tiles_occ[slot] = std::max(1, occ);
     }
     const long long ctas = std::min<long long>(ta.ntiles, (long long)v->num_sms * v->tiles_occ[slot]);
-    k_tile_desc<NCH, NW, kZ1><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->stream>>>(ta, const_cast<TileDesc*>(ta.desc));
+    if (v->prep_on_param) {
+        // (insert_common: the descriptors are built on param_stream right after the parameter
+        // upload, beside the previous step's fill / render; the kernels' stream waits for them)
+        k_tile_desc<NCH, NW, kZ1><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->param_stream>>>(ta, const_cast<TileDesc*>(ta.desc));
+        CK(cudaEventRecord(v->ev_prep, v->param_stream));
+        CK(cudaStreamWaitEvent(v->stream, v->ev_prep, 0));
+    } else {
+        k_tile_desc<NCH, NW, kZ1><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->stream>>>(ta, const_cast<TileDesc*>(ta.desc));
+    }
     k_pnn_tiles<NCH, NW, kBox, kZ1><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
     v->launches += 2;
     return SVR_OK;
@@ -1224,7 +1239,8 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                 CK(cudaMalloc(&v->d_work, sizeof(ull) * v->work_cap));
                 if (!v->d_work_n) CK(cudaMalloc(&v->d_work_n, sizeof(unsigned int)));
             }
-            CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int), v->stream));
+            CK(cudaMemsetAsync(v->d_work_n, 0, sizeof(unsigned int),
+                               v->prep_on_param && !fan_tiles ? v->param_stream : v->stream));
             if (fan_tiles) {
                 if (int e = launch_fan(v, box, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats)) return e;
             } else {
@@ -1328,6 +1344,9 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
     cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(v->stream, &cap_st));
     if (cap_st == cudaStreamCaptureStatusNone) {
+        // (after the previous call's insert kernels: they read d_params2[other], the descriptor
+        // buffer and the exact-pass work list this call's setup rewrites)
+        CK(cudaStreamWaitEvent(v->param_stream, v->ins_done, 0));
         CK(cudaStreamWaitEvent(v->param_stream, v->params_used[v->pslot], 0));
         CK(cudaMemcpyAsync(v->d_params, hp, sizeof(FrameParams) * n, cudaMemcpyHostToDevice,
                            v->param_stream));
@@ -1349,9 +1368,13 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
     }
     bool pinned = false;
     if (is_device_ptr(px, &pinned)) {
+        // one launch chunk (<= 65535 frames) off a capture: K1's setup goes to param_stream too
+        v->prep_on_param = cap_st == cudaStreamCaptureStatusNone && n <= 65535;
         const int e = insert_device(v, mode, px, pitch, fstride, w, h, n, v->d_params, cal, skip_zero,
                                     want_box, boxes, mark, tag, stats);
+        v->prep_on_param = false;
         CK(cudaEventRecord(v->params_used[v->pslot], v->stream));
+        CK(cudaEventRecord(v->ins_done, v->stream));
         return e;
     }
     // host frames: double-buffered pinned staging, H2D on copy_stream overlapped with kernels
@@ -1400,6 +1423,7 @@ static int insert_common(svr_volume* v, int mode, const uint8_t* px, int64_t pit
         CK(cudaEventRecord(v->ev_free[b], v->stream));
     }
     CK(cudaEventRecord(v->params_used[v->pslot], v->stream));
+    CK(cudaEventRecord(v->ins_done, v->stream));
     return SVR_OK;
 }
 
