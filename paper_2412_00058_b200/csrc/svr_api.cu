@@ -118,6 +118,7 @@ struct svr_volume {
     cudaEvent_t params_used[2] = {nullptr, nullptr};  // last kernel reading d_params2[i] done
     cudaEvent_t ins_done = nullptr;   // the last insert call's kernels done (param_stream waits)
     cudaEvent_t ev_prep = nullptr;    // param_stream's share of the current call done
+    cudaEvent_t ev_tiles_up = nullptr;  // upload_tiles' H2D on param_stream done
     bool prep_on_param = false;       // insert_common: K1's per-tile setup goes to param_stream
     int params_cap = 0;
     int pslot = 0;
@@ -767,6 +768,7 @@ extern "C" int svr_destroy(svr_volume* v) {
     }
     if (v->ins_done) cudaEventDestroy(v->ins_done);
     if (v->ev_prep) cudaEventDestroy(v->ev_prep);
+    if (v->ev_tiles_up) cudaEventDestroy(v->ev_tiles_up);
     if (v->own_stream && v->stream) cudaStreamDestroy(v->stream);
     if (v->own_stream_saved) cudaStreamDestroy(v->own_stream_saved);
     if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
@@ -827,6 +829,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ins_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_prep, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_tiles_up, cudaEventDisableTiming);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&v->ev_ready[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&v->ev_free[i], cudaEventDisableTiming);
@@ -1517,7 +1520,17 @@ static int upload_tiles(svr_volume* v, const void* host, size_t bytes, void** de
         v->tiles_cap = cap;
     }
     std::memcpy(v->h_tiles[s], host, bytes);
-    CK(cudaMemcpyAsync(v->d_tiles[s], v->h_tiles[s], bytes, cudaMemcpyHostToDevice, v->stream));
+    // (off a capture: the small H2D goes on param_stream -- the slot's consumers are done, see
+    // above -- so it does not queue behind the kernels already on v->stream)
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(v->stream, &cap_st));
+    if (cap_st == cudaStreamCaptureStatusNone) {
+        CK(cudaMemcpyAsync(v->d_tiles[s], v->h_tiles[s], bytes, cudaMemcpyHostToDevice, v->param_stream));
+        CK(cudaEventRecord(v->ev_tiles_up, v->param_stream));
+        CK(cudaStreamWaitEvent(v->stream, v->ev_tiles_up, 0));
+    } else {
+        CK(cudaMemcpyAsync(v->d_tiles[s], v->h_tiles[s], bytes, cudaMemcpyHostToDevice, v->stream));
+    }
     v->tiles_prev = s;
     v->tiles_prev_stream = v->stream;
     *dev = v->d_tiles[s];
