@@ -295,6 +295,9 @@ struct PrepCtx {
 // A launch's shape carries bit 2 (kShapeZ1) when every frame has at most one y and one z carry
 // per chunk (FrameParams::lin_fit bit 4): the kZ1 walk variant.
 constexpr int kShapeZ1 = 4, kFitZ1 = 16;
+#ifndef SVR_WORK_CTAS_PER_SM
+#define SVR_WORK_CTAS_PER_SM 2  // k_pnn_work grid cap (the list holds ~1 chunk per frame)
+#endif
 #ifndef SVR_FILL_TY
 #define SVR_FILL_TY 8  // batch fill: rows per warp of k_fill_warp
 #endif
@@ -1228,7 +1231,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
         int* bx = boxes ? boxes + 6 * k0 : nullptr;
         // the deferred-chunk pass is grid-strided over a worklist of a few entries per frame:
         // a single frame must not pay for launching thousands of idle CTAs
-        const int work_ctas = std::min(4096, std::max(16, 8 * m));
+        const int work_ctas = std::min(SVR_WORK_CTAS_PER_SM * v->num_sms, std::max(16, 8 * m));
         const GridDev gd = dev_grid(v->d);
         if (shape >= 0 || fan_tiles) {
             // k_pnn_tiles / k_fan_tiles defer whole chunks with no overflow path: room for every chunk
