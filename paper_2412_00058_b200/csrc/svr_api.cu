@@ -298,6 +298,9 @@ constexpr int kShapeZ1 = 4, kFitZ1 = 16;
 #ifndef SVR_WORK_CTAS_PER_SM
 #define SVR_WORK_CTAS_PER_SM 2  // k_pnn_work grid cap (the list holds ~1 chunk per frame)
 #endif
+#ifndef SVR_FILL_ZC
+#define SVR_FILL_ZC 32  // batch fill: planes per k_fill_warp march (fewer when the grid is small)
+#endif
 #ifndef SVR_FILL_TY
 #define SVR_FILL_TY 8  // batch fill: rows per warp of k_fill_warp
 #endif
@@ -1568,7 +1571,7 @@ static int fill_boxes(svr_volume* v, const std::vector<Box>& bs, int32_t mode, i
         };
         // planes per march: 32, unless that leaves fewer than ~8 CTAs per SM (a slab's share of a
         // multi-GPU split, small incremental boxes): then 16 or 8
-        int zc = 32;
+        int zc = SVR_FILL_ZC;
         tile(zc);
         const long long want = 8ll * v->num_sms;
         while (zc > 8 && total < want) {
