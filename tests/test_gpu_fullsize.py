@@ -249,3 +249,37 @@ def test_cfg5_trilinear_gigabyte_slab_vs_oracle():
     np.testing.assert_allclose(mean, rmean, rtol=1e-5, atol=0)
     np.testing.assert_allclose(mx, rmx, rtol=1e-5, atol=0)
     grid.close()
+
+
+def test_walk_variants_kz1_and_general_and_mixed():
+    """K1 has two walks (svr_k1.cuh): kZ1 for frames with at most one y and one z carry per
+    16-pixel chunk (z move as a predicated add, y / z ties captured at their carry) and the
+    general one.  Frames rotated 40 degrees about z take the general walk (15 |Dc_y| > 1), small
+    rotations the kZ1 walk, a mixed batch the general walk for all; every case stays bit-exact
+    through the tile table, and the per-frame graph re-captures when a frame leaves its variant."""
+    v = 0.5
+    small = [(_rot((0.2, 0.1, 1.0), 3.0 * k - 6.0), (10.0 + 0.4 * k, 6.0, 8.0 + 0.45 * k)) for k in range(5)]
+    big = [(_rot((0.05, 0.1, 1.0), 40.0 + 2.0 * k), (30.0 + 0.3 * k, 4.0, 9.0 + 0.5 * k)) for k in range(5)]
+    def dcy_chunk(q):  # 15 |Dc_y| of a pose (identity calibration): the y fraction's chunk span
+        w, x, y, z = q
+        r10 = 2.0 * (x * y + w * z)  # R[1][0]: the image column direction's y component
+        return 15.0 * abs(r10) * 0.1 / v
+    assert all(dcy_chunk(q) < 1.0 for q, _ in small) and all(dcy_chunk(q) > 1.0 for q, _ in big)
+    for name, poses in (("kz1", small), ("general", big), ("mixed", small[:3] + big[:3])):
+        wl = _workload(name, 128, 256, 0.1, 0.1, v, (96, 96, 48), (0.0, 0.0, 0.0), poses)
+        st, st1 = _check_vs_oracle(wl, what=name)
+        assert st["tiles_table"] > 0 and st1["tiles_table"] > 0, name
+    # the per-frame graph: kZ1 frames, then general ones (re-capture), then kZ1 again
+    wl = _workload("alt", 128, 256, 0.1, 0.1, v, (96, 96, 48), (0.0, 0.0, 0.0), small[:2] + big[:2] + small[2:4])
+    frames = wl.frames_np()
+    grid = _grid(wl)
+    rp = synth.render_params(depth_lo_mm=1.0, depth_hi_mm=12.0, band_above_mm=1.0, band_below_mm=0.5)
+    for k in range(wl.nframes):
+        grid.frame_step(frames[k], wl.poses[k:k + 1], wl.calib, 1, rp)
+    grid.sync()
+    ref = O.OracleGrid.for_workload(wl)
+    for k in range(wl.nframes):
+        ref.insert_frame(frames[k], wl.poses[k:k + 1], wl.calib)
+    _assert_acc(grid, ref, "alternating per-frame graph")
+    assert grid.stats()["graph_captures"] >= 2
+    grid.close()
