@@ -302,7 +302,7 @@ constexpr int kShapeZ1 = 4, kFitZ1 = 16;
 #define SVR_FILL_ZC 32  // batch fill: planes per k_fill_warp march (fewer when the grid is small)
 #endif
 #ifndef SVR_FILL_TY
-#define SVR_FILL_TY 8  // batch fill: rows per warp of k_fill_warp
+#define SVR_FILL_TY 6  // batch fill: rows per warp of k_fill_warp (A/B: 6 rows at 6 CTAs/SM beat 4, 5, 7, 8)
 #endif
 
 static inline int shape_cols(int s) { return (s & 1) ? 32 : 64; }
