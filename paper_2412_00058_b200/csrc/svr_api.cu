@@ -301,6 +301,9 @@ constexpr int kShapeZ1 = 4, kFitZ1 = 16;
 #ifndef SVR_FILL_ZC
 #define SVR_FILL_ZC 32  // batch fill: planes per k_fill_warp march (fewer when the grid is small)
 #endif
+#ifndef SVR_DEPTH_SEG
+#define SVR_DEPTH_SEG 2  // batch render: threads per (x, z) column of k_depth (A/B: 2 beat 4 and 8)
+#endif
 #ifndef SVR_FILL_TY
 #define SVR_FILL_TY 6  // batch fill: rows per warp of k_fill_warp (A/B: 6 rows at 6 CTAs/SM beat 4, 5, 7, 8)
 #endif
@@ -1725,7 +1728,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
         }
     }
     if (dt.empty()) return SVR_OK;
-    const long long nd = tile_cols(dt, 128 / 4), nm = tile_cols(mt);  // k_depth<4>: 4 threads per column
+    const long long nd = tile_cols(dt, 128 / SVR_DEPTH_SEG), nm = tile_cols(mt);  // k_depth<SEG>: SEG threads per column
     // one upload holds both tables: [dt | mt]
     std::vector<ColTiles> both(dt);
     both.insert(both.end(), mt.begin(), mt.end());
@@ -1735,7 +1738,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
     const ColTiles* dmt = ddt + dt.size();
     const GridDev g = dev_grid(v->d);
     if (v->tri) {  // trilinear volume: f = wsum / weight, no fill layer
-        k_depth<4, true><<<grid_1d(nd), 128, 0, v->stream>>>(nullptr, nullptr, g, ddt, (int)dt.size(), ylo,
+        k_depth<SVR_DEPTH_SEG, true><<<grid_1d(nd), 128, 0, v->stream>>>(nullptr, nullptr, g, ddt, (int)dt.size(), ylo,
                                                               yhi, p->fill_mode, v->r_depth, v->tri);
         v->launches++;
         CKL();
@@ -1747,7 +1750,7 @@ static int render_boxes(svr_volume* v, const svr_box* dirty, int n, int32_t fill
         CKL();
         return SVR_OK;
     }
-    k_depth<4><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
+    k_depth<SVR_DEPTH_SEG><<<grid_1d(nd), 128, 0, v->stream>>>(v->acc, v->fill, g, ddt, (int)dt.size(), ylo, yhi,
                                                     p->fill_mode, v->r_depth);
     v->launches++;
     CKL();
