@@ -261,8 +261,11 @@ __device__ __forceinline__ void fan_box(BoxAcc& bb, const long long (&A)[3], con
 // their buffer words zeroed again (a tie chunk's runs are just dropped: nothing to undo).  The
 // tile after next's scanline constants and descriptor are staged with cp.async; the next tile's
 // pixels are loaded before the current tile's flush.
+#ifndef SVR_FAN_MINB
+#define SVR_FAN_MINB 8  // k_fan_tiles: CTAs per SM the register budget is cut for (A/B: 8 beat 6, 7; 7 fit by shared memory)
+#endif
 template <bool kBox>
-__global__ void __launch_bounds__(128, SVR_TILES_MINB) k_fan_tiles(const FanArgs fa) {
+__global__ void __launch_bounds__(128, SVR_FAN_MINB) k_fan_tiles(const FanArgs fa) {
     constexpr int NW = 4, NCH = 2, NT = 32 * NW, TCOLS = 16 * NCH * NW;
     static_assert(15 * NT * 8 <= 4 * kTabWords, "run buffer: 15 entries per thread in the table memory");
     __shared__ __align__(16) uint32_t s_tab[kTabWords];

@@ -34,7 +34,7 @@
 #define SVR_TILES_PREFETCH 0  // k_pnn_tiles: L2 prefetch of each row's first voxel line (A/B: 0.571 vs 0.565 ms without)
 #endif
 #ifndef SVR_TILES_MINB
-#define SVR_TILES_MINB 7  // k_pnn_tiles (128 threads): CTAs per SM the register budget is cut for
+#define SVR_TILES_MINB 6  // k_pnn_tiles (128 threads): CTAs per SM the register budget is cut for (A/B: 6 beat 7, 8)
 #endif
 
 namespace svr {

@@ -1,2 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
-bash tools/_ab.sh
+bash tools/_ab_cfg.sh cfg3
