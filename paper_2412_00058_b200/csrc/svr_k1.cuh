@@ -33,6 +33,9 @@
 #ifndef SVR_TILES_PREFETCH
 #define SVR_TILES_PREFETCH 0  // k_pnn_tiles: L2 prefetch of each row's first voxel line (A/B: 0.571 vs 0.565 ms without)
 #endif
+#ifndef SVR_FLUSH_UNROLL
+#define SVR_FLUSH_UNROLL 1  // k_pnn_tiles flush loop unroll
+#endif
 #ifndef SVR_TILES_MINB
 #define SVR_TILES_MINB 6  // k_pnn_tiles (128 threads): CTAs per SM the register budget is cut for (A/B: 6 beat 7, 8)
 #endif
@@ -44,6 +47,7 @@ namespace svr {
 // z step XORs its bit 14: plane 0 spans [tab, tab + 8 KB) with tab < 8 KB (static shared memory
 // starts at the CTA's 1 KB reserved area; checked per CTA), so bit 14 is 0 there and 1 in plane 1.
 // kTabStr is odd, so rows 1-2 voxels apart (a warp's lanes) fall into distinct banks.
+constexpr int kFlushUnroll = SVR_FLUSH_UNROLL;
 constexpr int kTabStr = 33;                    // table row stride in words
 constexpr int kTabPlane = 4096;                // words between the parity planes (bit 14)
 constexpr int kTabMaxY = 62;                   // voxel rows (62 * 33 <= 2048 words per plane)
@@ -524,6 +528,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 float yf = (float)yr;
                 const int dti = kTabStr * R;
                 const uint32_t dgo = (uint32_t)R * nx8;
+#pragma unroll kFlushUnroll
                 for (int y = yr; y < Y; y += R) {
                     const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + TG::kPlane];
                     s_tab[ti] = 0u;
