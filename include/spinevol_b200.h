@@ -18,7 +18,9 @@
  *     plus 5 for CUDA/NCCL failures.  No C++ exception crosses this boundary.
  *   - Buffers are owned by the caller and may be host (pageable or pinned) or device
  *     pointers; the library detects which.  Device memory of a volume is owned by
- *     the handle.  Calls on one handle are serialised onto the handle's stream.
+ *     the handle.  Calls on one handle are serialised onto the handle's stream (their small
+ *     uploads run on an internal stream joined to it by events: an event recorded on the
+ *     handle's stream after a call, or svr_sync, covers all of the call's work).
  *   - Voxel layout: x fastest, then y, then z.  A handle holds the
  *     global z planes [z_begin, z_end) (a slab; the whole grid when z_begin=0,
  *     z_end=nz).  All boxes are in GLOBAL voxel indices, inclusive.
