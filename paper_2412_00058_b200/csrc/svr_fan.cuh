@@ -264,6 +264,9 @@ __device__ __forceinline__ void fan_box(BoxAcc& bb, const long long (&A)[3], con
 #ifndef SVR_FAN_MINB
 #define SVR_FAN_MINB 8  // k_fan_tiles: CTAs per SM the register budget is cut for (A/B: 8 beat 6, 7; 7 fit by shared memory)
 #endif
+#ifndef SVR_FAN_ORDER
+#define SVR_FAN_ORDER 0  // k_fan_tiles tile order: 0 frame-major, 1 tile-major (frames fastest)
+#endif
 template <bool kBox>
 __global__ void __launch_bounds__(128, SVR_FAN_MINB) k_fan_tiles(const FanArgs fa) {
     constexpr int NW = 4, NCH = 2, NT = 32 * NW, TCOLS = 16 * NCH * NW;
@@ -288,26 +291,45 @@ __global__ void __launch_bounds__(128, SVR_FAN_MINB) k_fan_tiles(const FanArgs f
     // consecutive tiles (a few dozen frames), so neighbouring frames' adds to the same voxels
     // meet in L2 instead of each reading the voxel's sector from HBM
     const long long t0 = blockIdx.x, tstep = gridDim.x, t1 = fa.ntiles;
-    // (frame, tile row, tile column) of tile t, advanced by tstep without divisions per tile
-    const int sf = (int)(tstep / tpf), sr = (int)(tstep - (long long)sf * tpf);
-    const int sy = sr / fa.ntx, sx = sr - sy * fa.ntx;
+    // (frame, tile row, tile column) of tile t, advanced by tstep without divisions per tile: a
+    // mixed-radix counter of digits a0 (fastest, radix R0), a1 (R1), a2.  Frame-major order: a0 =
+    // tile column, a1 = tile row, a2 = frame.  Tile-major (SVR_FAN_ORDER 1): a0 = frame, a1 = tile
+    // column, a2 = tile row -- the CTAs in flight work on one fan patch of consecutive frames
+#if SVR_FAN_ORDER
+    const int R0 = (int)(t1 / tpf), R1 = fa.ntx;
+#else
+    const int R0 = fa.ntx, R1 = fa.nty;
+#endif
+    const long long R01 = (long long)R0 * R1;
+    const int s2 = (int)(tstep / R01), sr = (int)(tstep - (long long)s2 * R01);
+    const int s1 = sr / R0, s0 = sr - s1 * R0;
     auto split = [&](long long t, int& fq, int& tyq, int& txq) {
-        fq = (int)(t / tpf);
-        const int r = (int)(t - (long long)fq * tpf);
-        tyq = r / fa.ntx;
-        txq = r - tyq * fa.ntx;
+#if SVR_FAN_ORDER
+        int& a0 = fq; int& a1 = txq; int& a2 = tyq;
+#else
+        int& a0 = txq; int& a1 = tyq; int& a2 = fq;
+#endif
+        a2 = (int)(t / R01);
+        const int r = (int)(t - (long long)a2 * R01);
+        a1 = r / R0;
+        a0 = r - a1 * R0;
     };
     auto advance = [&](int& fq, int& tyq, int& txq) {
-        txq += sx;
-        tyq += sy;
-        fq += sf;
-        if (txq >= fa.ntx) {
-            txq -= fa.ntx;
-            ++tyq;
+#if SVR_FAN_ORDER
+        int& a0 = fq; int& a1 = txq; int& a2 = tyq;
+#else
+        int& a0 = txq; int& a1 = tyq; int& a2 = fq;
+#endif
+        a0 += s0;
+        a1 += s1;
+        a2 += s2;
+        if (a0 >= R0) {
+            a0 -= R0;
+            ++a1;
         }
-        if (tyq >= fa.nty) {
-            tyq -= fa.nty;
-            ++fq;
+        if (a1 >= R1) {
+            a1 -= R1;
+            ++a2;
         }
     };
     int f, ty, tx;

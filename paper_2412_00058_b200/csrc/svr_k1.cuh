@@ -33,6 +33,9 @@
 #ifndef SVR_TILES_PREFETCH
 #define SVR_TILES_PREFETCH 0  // k_pnn_tiles: L2 prefetch of each row's first voxel line (A/B: 0.571 vs 0.565 ms without)
 #endif
+#ifndef SVR_K1_ORDER
+#define SVR_K1_ORDER 0  // k_pnn_tiles tile order: 0 frame-major, 1 tile-major (frames fastest)
+#endif
 #ifndef SVR_FLUSH_UNROLL
 #define SVR_FLUSH_UNROLL 1  // k_pnn_tiles flush loop unroll
 #endif
@@ -112,23 +115,45 @@ __device__ __forceinline__ void tile_step(uint32_t& w0, uint32_t& w1, uint32_t& 
 
 // kZ1 step (at most one y and one z carry per chunk, tile_shapes_fit): the z move is +-16 KB
 // (dz, fixed per chunk by its start parity) as a predicated add, which ptxas puts on the FMA pipe
-// like the x and y moves -- the walk is ALU-bound (carries, tie screen, PRMT); where y or z carries
-// its new (post-carry) fraction is captured into ty / tz with a predicated multiply by an opaque
-// 1 (an FMA-pipe move; a tie in y or z can only sit at the chunk start or right after its one
-// carry), so the per-pixel tie screen needs only x on the ALU pipe
-__device__ __forceinline__ void tile_step_cap(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
-                                              uint32_t& ty, uint32_t& tz, uint32_t e0, uint32_t e1,
-                                              uint32_t e2, uint32_t sx, uint32_t sy, uint32_t dz,
-                                              uint32_t one) {
+// like the x and y moves -- the walk is ALU-bound (carries, tie screen, PRMT).  A tie in y or z can
+// only sit at the chunk start (screened there) or right after the axis' one carry; that post-carry
+// fraction is recovered after the chunk from the final one (carry_residue), so the per-pixel tie
+// screen needs only x.
+__device__ __forceinline__ void tile_step_z1(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& a,
+                                             uint32_t e0, uint32_t e1, uint32_t e2, uint32_t sx,
+                                             uint32_t sy, uint32_t dz) {
     asm("{\n\t.reg .pred p0, p1, p2;\n\t.reg .u32 c0, c1, c2;\n\t"
-        "add.cc.u32 %0, %0, %6;\n\taddc.u32 c0, 0, 0;\n\t"
-        "add.cc.u32 %1, %1, %7;\n\taddc.u32 c1, 0, 0;\n\t"
-        "add.cc.u32 %2, %2, %8;\n\taddc.u32 c2, 0, 0;\n\t"
+        "add.cc.u32 %0, %0, %4;\n\taddc.u32 c0, 0, 0;\n\t"
+        "add.cc.u32 %1, %1, %5;\n\taddc.u32 c1, 0, 0;\n\t"
+        "add.cc.u32 %2, %2, %6;\n\taddc.u32 c2, 0, 0;\n\t"
         "setp.ne.u32 p0, c0, 0;\n\tsetp.ne.u32 p1, c1, 0;\n\tsetp.ne.u32 p2, c2, 0;\n\t"
-        "@p0 add.u32 %3, %3, %9;\n\t@p1 add.u32 %3, %3, %10;\n\t@p2 add.u32 %3, %3, %11;\n\t"
-        "@p1 mul.lo.u32 %4, %1, %12;\n\t@p2 mul.lo.u32 %5, %2, %12;\n\t}"
-        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a), "+r"(ty), "+r"(tz)
-        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "r"(dz), "r"(one));
+        "@p0 add.u32 %3, %3, %7;\n\t@p1 add.u32 %3, %3, %8;\n\t@p2 add.u32 %3, %3, %9;\n\t}"
+        : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(a)
+        : "r"(e0), "r"(e1), "r"(e2), "r"(sx), "r"(sy), "r"(dz));
+}
+
+// The post-carry fraction of an axis that carried at most once in a chunk, from its final fraction
+// w: the fractions after the carry are w_c, w_c + e, ..., w = w_c + m e with 0 <= w_c < e, so w_c =
+// w mod e.  The quotient m <= 15 comes from fp32 (relative error ~2^-21, so it is off only when w / e
+// sits within ~1e-5 of a half-integer, far from a tie) and the residue w - m e is exact modulo 2^32:
+// where w_c is in the tie window the result is w_c exactly; otherwise it is >= the window (or wraps
+// to a huge value).  Only called for an axis that carried in the chunk (its final fraction wrapped
+// below the start one).  rcp = 1 / e.
+__device__ __forceinline__ uint32_t carry_residue(uint32_t w, uint32_t e, float rcp) {
+    const uint32_t m = (uint32_t)__float2int_rn(__uint2float_rn(w) * rcp);
+    return w - m * e;
+}
+
+#ifndef SVR_PX_DP4A
+#define SVR_PX_DP4A 1  // pixel word as IDP.4A (FMA pipe) instead of PRMT (ALU pipe, the walk's limit)
+#endif
+// table add of byte k of w: the byte + o20 (count 1 << 20 for a chunk that writes, 0 otherwise)
+__device__ __forceinline__ uint32_t px_word(uint32_t w, int k, uint32_t o20) {
+#if SVR_PX_DP4A
+    return __dp4a(w, 1u << (8 * k), o20);
+#else
+    return __byte_perm(w, o20, 0x7640 | k);
+#endif
 }
 
 // A frame's constants (k_tile_desc writes one per frame), staged in shared memory with each
@@ -213,7 +238,7 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
         fr.sy = fp.Dc[1] < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
         fr.p1 = (float)fp.pz[1];
         fr.p2 = (float)fp.pz[2];
-        fr.pad = 1u;  // (an opaque 1: tile_step_cap's predicated moves)
+        fr.pad = 0u;
         ta.frc[f] = fr;
     }
 }
@@ -284,30 +309,48 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
     // consecutive tiles (a few dozen frames), so neighbouring frames' adds to the same voxels
     // meet in L2 instead of each reading the voxel's sector from HBM
     const long long t0 = blockIdx.x, tstep = gridDim.x, t1 = ta.ntiles;
-    __shared__ int s_adv[3];  // tstep as (frames, tile rows, tile columns)
+    // tile t as a mixed-radix counter of digits a0 (fastest, radix R0), a1 (R1), a2, advanced by
+    // tstep without divisions.  Frame-major order: a0 = tile column, a1 = tile row, a2 = frame;
+    // tile-major (SVR_K1_ORDER 1): a0 = frame, a1 = tile column, a2 = tile row
+#if SVR_K1_ORDER
+    const int R0 = (int)(t1 / tpf), R1 = ta.ntx;
+#define SVR_K1_DIGITS(fq, tyq, txq) int& a0 = fq; int& a1 = txq; int& a2 = tyq
+#else
+    const int R0 = ta.ntx, R1 = ta.nty;
+#define SVR_K1_DIGITS(fq, tyq, txq) int& a0 = txq; int& a1 = tyq; int& a2 = fq
+#endif
+    const long long R01 = (long long)R0 * R1;
+    __shared__ int s_adv[3];  // tstep as (a0, a1, a2) digits
     if (tid == 0) {
-        const int sf = (int)(tstep / tpf), sr = (int)(tstep - (long long)sf * tpf);
+        const int sf = (int)(tstep / R01), sr = (int)(tstep - (long long)sf * R01);
         s_adv[0] = sf;
-        s_adv[1] = sr / ta.ntx;
-        s_adv[2] = sr - s_adv[1] * ta.ntx;
+        s_adv[1] = sr / R0;
+        s_adv[2] = sr - s_adv[1] * R0;
     }
     __syncthreads();
     auto advance = [&](int& fq, int& tyq, int& txq) {  // tile + tstep, without divisions
-        txq += s_adv[2];
-        tyq += s_adv[1];
-        fq += s_adv[0];
-        if (txq >= ta.ntx) {
-            txq -= ta.ntx;
-            ++tyq;
+        SVR_K1_DIGITS(fq, tyq, txq);
+        a0 += s_adv[2];
+        a1 += s_adv[1];
+        a2 += s_adv[0];
+        if (a0 >= R0) {
+            a0 -= R0;
+            ++a1;
         }
-        if (tyq >= ta.nty) {
-            tyq -= ta.nty;
-            ++fq;
+        if (a1 >= R1) {
+            a1 -= R1;
+            ++a2;
         }
     };
-    int f = (int)(t0 / tpf);
-    int rem = (int)(t0 - (long long)f * tpf);
-    int ty = rem / ta.ntx, tx = rem - ty * ta.ntx;
+    int f, ty, tx;
+    {
+        SVR_K1_DIGITS(f, ty, tx);
+        a2 = (int)(t0 / R01);
+        const int r = (int)(t0 - (long long)a2 * R01);
+        a1 = r / R0;
+        a0 = r - a1 * R0;
+    }
+#undef SVR_K1_DIGITS
     int cur_f = -1;
     unsigned int ntiles_cta = 0;
     int slot = 0;
@@ -430,7 +473,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         if (tok && warp < S) {
             const uint32_t e0 = s_fr.E[0], e1 = s_fr.E[1], e2 = s_fr.E[2], sx = s_fr.sx, sy = s_fr.sy;
             const uint32_t tie2 = 2u * s_fr.te2;
-            const uint32_t one = s_fr.pad;  // (kZ1: tile_step_cap's opaque 1)
+            // (kZ1: 1 / e for the post-carry residues; MUFU accuracy suffices, see carry_residue)
+            const float rc1 = kZ1 ? __fdividef(1.0f, (float)e1) : 0.f, rc2 = kZ1 ? __fdividef(1.0f, (float)e2) : 0.f;
             // walk state at pixel 0 of the row
             uint32_t w0, w1, w2, a;
             {
@@ -448,27 +492,30 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 if (c > 0) tile_step<TG::kBit>(w0, w1, w2, a, e0, e1, e2, sx, sy);
                 const uint32_t o20 = (wmask >> c) & 1u ? 0x00100000u : 0u;
                 uint32_t tmin = min(w0, min(w1, w2));
-                red_shared(a, __byte_perm(wd[c][0], o20, 0x7640));
+                red_shared(a, px_word(wd[c][0], 0, o20));
                 if (kZ1) {
                     // at most one y and one z carry in the chunk: the z move is the fixed step to
                     // the other parity plane (an add on the FMA pipe instead of an ALU XOR)
                     const uint32_t dz = (a & (uint32_t)TG::kBit) ? 0u - (uint32_t)TG::kBit : (uint32_t)TG::kBit;
                     // y and z ties can only sit at the chunk start (screened above) or right after
-                    // their one carry: those fractions are captured, so per pixel only x is screened
-                    uint32_t ty = 0xffffffffu, tz = 0xffffffffu;
+                    // their one carry: recovered after the walk, so per pixel only x is screened
+                    const uint32_t w1s = w1, w2s = w2;
 #pragma unroll
                     for (int j = 1; j < kChunk; ++j) {
-                        tile_step_cap(w0, w1, w2, a, ty, tz, e0, e1, e2, sx, sy, dz, one);
+                        tile_step_z1(w0, w1, w2, a, e0, e1, e2, sx, sy, dz);
                         tmin = min(tmin, w0);
-                        red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                        red_shared(a, px_word(wd[c][j >> 2], j & 3, o20));
                     }
-                    tmin = min(tmin, min(ty, tz));
+                    // (only where the axis carried: w wrapped below its chunk-start value)
+                    const uint32_t ry = w1 < w1s ? carry_residue(w1, e1, rc1) : 0xffffffffu;
+                    const uint32_t rz = w2 < w2s ? carry_residue(w2, e2, rc2) : 0xffffffffu;
+                    tmin = min(tmin, min(ry, rz));
                 } else {
 #pragma unroll
                     for (int j = 1; j < kChunk; ++j) {
                         tile_step<TG::kBit>(w0, w1, w2, a, e0, e1, e2, sx, sy);
                         tmin = min(tmin, min(w0, min(w1, w2)));
-                        red_shared(a, __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                        red_shared(a, px_word(wd[c][j >> 2], j & 3, o20));
                     }
                 }
                 const bool tie = o20 != 0u && tmin < tie2;
@@ -476,11 +523,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                     if (tie) {
                         uint32_t v0, v1, v2, ua;  // state at the chunk's pixel 0 (= the walk's)
                         walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, (uint32_t)TG::kBit, v0, v1, v2, ua);
-                        red_shared(ua, 0u - __byte_perm(wd[c][0], o20, 0x7640));
+                        red_shared(ua, 0u - px_word(wd[c][0], 0, o20));
 #pragma unroll
                         for (int j = 1; j < kChunk; ++j) {  // (unrolled: wd stays in registers)
                             tile_step<TG::kBit>(v0, v1, v2, ua, e0, e1, e2, sx, sy);
-                            red_shared(ua, 0u - __byte_perm(wd[c][j >> 2], o20, 0x7640 | (j & 3)));
+                            red_shared(ua, 0u - px_word(wd[c][j >> 2], j & 3, o20));
                         }
                         push_work(ta, f, row, (c0t >> 4) + c);
                         atomicAdd(&s_cnt[1], 1u);

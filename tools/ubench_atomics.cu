@@ -32,6 +32,12 @@ __global__ void __launch_bounds__(256) kern(unsigned long long* g, int iters, un
         if (MODE == 7) atomicAdd(&g[key & ((1u << 25) - 1)], 1ull);             // 256 MiB window
         if (MODE == 8)  // warp-local: lanes within 64 words of a per-warp random base (sector sharing)
             atomicAdd(&g[((hash32((t >> 5) * 31u + it) & ((1u << 25) - 1)) + (hash32(t + it) & 63u)) & ((1u << 25) - 1)], 1ull);
+        if (MODE == 9)  // a warp's lanes on 32 consecutive words (8 sectors) at a random base, 1 MiB window
+            atomicAdd(&g[((hash32((t >> 5) * 31u + it) << 5) + lane) & ((1u << 17) - 1)], 1ull);
+        if (MODE == 10)  // the same in a 256 MiB window
+            atomicAdd(&g[((hash32((t >> 5) * 31u + it) << 5) + lane) & ((1u << 25) - 1)], 1ull);
+        if (MODE == 11)  // 2 lanes per word, 16 consecutive words (4 sectors), 1 MiB window
+            atomicAdd(&g[((hash32((t >> 5) * 31u + it) << 5) + (lane >> 1)) & ((1u << 17) - 1)], 1ull);
     }
     __syncthreads();
     if (MODE >= 2 && threadIdx.x == 0) sink[blockIdx.x] = s[lane];
@@ -71,6 +77,9 @@ int main() {
     run<6>("red64_same8", g, sink, blocks, iters);
     run<7>("red64_256MiB", g, sink, blocks, iters);
     run<8>("red64_warp64w", g, sink, blocks, iters);
+    run<9>("red64_coal_1MiB", g, sink, blocks, iters);
+    run<10>("red64_coal_256M", g, sink, blocks, iters);
+    run<11>("red64_pair_1MiB", g, sink, blocks, iters);
     cudaError_t e = cudaDeviceSynchronize();
     printf("status %s, SMs %d\n", cudaGetErrorString(e), sms);
     return e == cudaSuccess ? 0 : 1;
