@@ -36,6 +36,9 @@
 #ifndef SVR_K1_ORDER
 #define SVR_K1_ORDER 0  // k_pnn_tiles tile order: 0 frame-major, 1 tile-major (frames fastest)
 #endif
+#ifndef SVR_FLUSH_FMA
+#define SVR_FLUSH_FMA 0  // k_pnn_tiles flush: 1 = word split on the FMA pipe, 2 = + plane offsets by IMAD
+#endif
 #ifndef SVR_FLUSH_UNROLL
 #define SVR_FLUSH_UNROLL 1  // k_pnn_tiles flush loop unroll
 #endif
@@ -163,7 +166,7 @@ struct __align__(16) TileFrame {
     uint32_t E[3], neg[3];         // |Dc| low words; all-ones when Dc < 0 (mirrored fractions)
     uint32_t te2, sx, sy;          // tie window + 1; table byte steps along x and y
     float p1, p2;                  // frame plane slopes (FrameParams::pz[1], pz[2])
-    uint32_t pad;                  // 1
+    uint32_t pad;                  // 4096 (opaque to ptxas)
 };
 static_assert(sizeof(TileFrame) == 96, "TileFrame is staged as 6 x 16 bytes");
 
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(128) k_tile_desc(const TilesArgs ta, TileDesc*
         fr.sy = fp.Dc[1] < 0 ? 0u - 4u * kTabStr : 4u * kTabStr;
         fr.p1 = (float)fp.pz[1];
         fr.p2 = (float)fp.pz[2];
-        fr.pad = 0u;
+        fr.pad = 4096u;  // (an opaque 2^12: the flush's FMA-pipe word split)
         ta.frc[f] = fr;
     }
 }
@@ -276,6 +279,15 @@ __device__ __forceinline__ void red_word(unsigned long long addr, uint32_t v) {
         "{\n\t.reg .b32 hi, lo;\n\t.reg .b64 w;\n\t"
         "shr.u32 hi, %1, 20;\n\tand.b32 lo, %1, 1048575;\n\t"
         "mov.b64 w, {lo, hi};\n\tred.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v) : "memory");
+}
+
+// the same with the split on the FMA pipe (hi = v * 2^12 >> 32, lo = v - hi * 2^20; k12 = 4096 and
+// km20 = -2^20 opaque to ptxas, which would otherwise strength-reduce to ALU shifts)
+__device__ __forceinline__ void red_word_nz_fma(unsigned long long addr, uint32_t v, uint32_t k12, uint32_t km20) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 hi, lo;\n\t.reg .b64 w;\n\t"
+        "setp.ne.u32 p, %1, 0;\n\tmul.hi.u32 hi, %1, %2;\n\tmad.lo.u32 lo, hi, %3, %1;\n\t"
+        "mov.b64 w, {lo, hi};\n\t@p red.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v), "r"(k12), "r"(km20) : "memory");
 }
 
 // the same, predicated on v != 0 inside the asm (no branch around the RED)
@@ -575,19 +587,36 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 float yf = (float)yr;
                 const int dti = kTabStr * R;
                 const uint32_t dgo = (uint32_t)R * nx8;
+#if SVR_FLUSH_FMA
+                const uint32_t k12 = s_fr.pad, km20 = 0u - (k12 << 8), nsxy8 = 0u - sxy8;
+#endif
 #pragma unroll kFlushUnroll
                 for (int y = yr; y < Y; y += R) {
                     const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + TG::kPlane];
                     s_tab[ti] = 0u;
                     s_tab[ti + TG::kPlane] = 0u;
                     const uint32_t k = (uint32_t)(int)ceilf(fmaf(p2, yf, ttx));  // k - kmin >= 0
+#if SVR_FLUSH_FMA >= 2
+                    // plane 0 holds z = k + o, plane 1 z = k + 1 - o (o = parity offset): offsets by IMAD
+                    const uint32_t o = (k ^ zpar) & 1u;
+                    const uint32_t kb = k * sxy8 + go;
+                    const unsigned long long ga0 = fbase + (o * sxy8 + kb), ga1 = fbase + (o * nsxy8 + (kb + sxy8));
+                    red_word_nz_fma(ga0, v0, k12, km20);
+                    red_word_nz_fma(ga1, v1, k12, km20);
+#else
                     const bool odd = ((k ^ zpar) & 1u) != 0u;
                     const unsigned long long a0 = fbase + (k * sxy8 + go);
                     // per slot: an empty slot's voxel may lie outside the slab (face tiles), and a
                     // RED of 0 would still pull its line into L2 and write it back
                     const uint32_t vlo = odd ? v1 : v0, vhi = odd ? v0 : v1;
+#if SVR_FLUSH_FMA
+                    red_word_nz_fma(a0, vlo, k12, km20);
+                    red_word_nz_fma(a0 + sxy8, vhi, k12, km20);
+#else
                     red_word_nz(a0, vlo);
                     red_word_nz(a0 + sxy8, vhi);
+#endif
+#endif
                     ti += dti;
                     go += dgo;
                     yf += Rf;
