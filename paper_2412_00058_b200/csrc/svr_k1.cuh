@@ -39,6 +39,9 @@
 #ifndef SVR_FLUSH_FMA
 #define SVR_FLUSH_FMA 0  // k_pnn_tiles flush: 1 = word split on the FMA pipe, 2 = + plane offsets by IMAD
 #endif
+#ifndef SVR_FLUSH_PIPE
+#define SVR_FLUSH_PIPE 0  // k_pnn_tiles flush: next position's table words loaded ahead; ceil by FADD.RU
+#endif
 #ifndef SVR_FLUSH_UNROLL
 #define SVR_FLUSH_UNROLL 1  // k_pnn_tiles flush loop unroll
 #endif
@@ -590,12 +593,37 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
 #if SVR_FLUSH_FMA
                 const uint32_t k12 = s_fr.pad, km20 = 0u - (k12 << 8), nsxy8 = 0u - sxy8;
 #endif
+#if SVR_FLUSH_PIPE
+                // software-pipelined: the next position's slots are read (and zeroed) before this
+                // position's REDs, so the LDS latency overlaps the previous position's tail
+                uint32_t n0 = 0u, n1 = 0u;
+                if (yr < Y) {
+                    n0 = s_tab[ti];
+                    n1 = s_tab[ti + TG::kPlane];
+                    s_tab[ti] = 0u;
+                    s_tab[ti + TG::kPlane] = 0u;
+                }
+#endif
 #pragma unroll kFlushUnroll
                 for (int y = yr; y < Y; y += R) {
+#if SVR_FLUSH_PIPE
+                    const uint32_t v0 = n0, v1 = n1;
+                    if (y + R < Y) {
+                        n0 = s_tab[ti + dti];
+                        n1 = s_tab[ti + dti + TG::kPlane];
+                        s_tab[ti + dti] = 0u;
+                        s_tab[ti + dti + TG::kPlane] = 0u;
+                    }
+                    // ceil by a round-up add of 1.5 * 2^23 (FADD.RU, full rate) instead of F2I.CEIL:
+                    // the sum lies in [2^23, 2^24) (ulp 1) for |t| < 2^22, so it rounds up to
+                    // 1.5 * 2^23 + ceil(t) exactly
+                    const uint32_t k = __float_as_uint(__fadd_ru(fmaf(p2, yf, ttx), 12582912.0f)) - 0x4b400000u;
+#else
                     const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + TG::kPlane];
                     s_tab[ti] = 0u;
                     s_tab[ti + TG::kPlane] = 0u;
                     const uint32_t k = (uint32_t)(int)ceilf(fmaf(p2, yf, ttx));  // k - kmin >= 0
+#endif
 #if SVR_FLUSH_FMA >= 2
                     // plane 0 holds z = k + o, plane 1 z = k + 1 - o (o = parity offset): offsets by IMAD
                     const uint32_t o = (k ^ zpar) & 1u;

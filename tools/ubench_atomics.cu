@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(256) kern(unsigned long long* g, int iters, un
     __syncthreads();
     unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned lane = threadIdx.x & 31;
+    unsigned long long acc = 0;
     for (int it = 0; it < iters; ++it) {
         unsigned key = (MODE == 1 || MODE == 3) ? hash32((t >> 2) * 977u + it) : hash32(t * 131u + it);
         if (MODE == 0 || MODE == 1) atomicAdd(&g[key & ((1u << 17) - 1)], 1ull);
@@ -38,9 +39,21 @@ __global__ void __launch_bounds__(256) kern(unsigned long long* g, int iters, un
             atomicAdd(&g[((hash32((t >> 5) * 31u + it) << 5) + lane) & ((1u << 25) - 1)], 1ull);
         if (MODE == 11)  // 2 lanes per word, 16 consecutive words (4 sectors), 1 MiB window
             atomicAdd(&g[((hash32((t >> 5) * 31u + it) << 5) + (lane >> 1)) & ((1u << 17) - 1)], 1ull);
+        // 2 GiB window (every sector misses L2): RED alone, RED after an L2 prefetch issued PF
+        // iterations earlier, plain loads, prefetches alone
+        constexpr unsigned W28 = (1u << 28) - 1;
+        if (MODE == 12) atomicAdd(&g[hash32(t * 131u + it) & W28], 1ull);
+        if (MODE == 13 || MODE == 15 || MODE == 16) {
+            constexpr int PF = MODE == 13 ? 8 : (MODE == 15 ? 2 : 32);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(&g[hash32(t * 131u + it + PF) & W28]));
+            atomicAdd(&g[hash32(t * 131u + it) & W28], 1ull);
+        }
+        if (MODE == 14) acc += g[hash32(t * 131u + it) & W28];
+        if (MODE == 17) asm volatile("prefetch.global.L2 [%0];" ::"l"(&g[hash32(t * 131u + it) & W28]));
     }
     __syncthreads();
-    if (MODE >= 2 && threadIdx.x == 0) sink[blockIdx.x] = s[lane];
+    if (MODE == 14 && acc == 0x123456789ull) sink[t] = acc;
+    if (MODE >= 2 && MODE < 12 && threadIdx.x == 0) sink[blockIdx.x] = s[lane];
 }
 
 template <int MODE>
@@ -62,9 +75,9 @@ float run(const char* name, unsigned long long* g, unsigned long long* sink, int
 
 int main() {
     unsigned long long *g, *sink;
-    cudaMalloc(&g, sizeof(unsigned long long) << 25);
+    cudaMalloc(&g, sizeof(unsigned long long) << 28);
     cudaMalloc(&sink, sizeof(unsigned long long) << 20);
-    cudaMemset(g, 0, sizeof(unsigned long long) << 25);
+    cudaMemset(g, 0, sizeof(unsigned long long) << 28);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     int blocks = sms * 8, iters = 512;
@@ -80,6 +93,12 @@ int main() {
     run<9>("red64_coal_1MiB", g, sink, blocks, iters);
     run<10>("red64_coal_256M", g, sink, blocks, iters);
     run<11>("red64_pair_1MiB", g, sink, blocks, iters);
+    run<12>("red64_2GiB", g, sink, blocks, iters);
+    run<15>("red64_2GiB_pf2", g, sink, blocks, iters);
+    run<13>("red64_2GiB_pf8", g, sink, blocks, iters);
+    run<16>("red64_2GiB_pf32", g, sink, blocks, iters);
+    run<14>("ld64_2GiB", g, sink, blocks, iters);
+    run<17>("pf_2GiB", g, sink, blocks, iters);
     cudaError_t e = cudaDeviceSynchronize();
     printf("status %s, SMs %d\n", cudaGetErrorString(e), sms);
     return e == cudaSuccess ? 0 : 1;
