@@ -155,6 +155,7 @@ struct svr_volume {
     size_t tiles_cap = 0;
     unsigned int* d_work_n = nullptr;
     unsigned int work_cap = 0;
+    int tri_kernel = 0;         // SVR_TRI_KERNEL=chunk: trilinear splat through k_insert (cross-check)
     int insert_kernel = 3;      // SVR_INSERT_KERNEL=direct: every PNN insert through k_insert (the
                                 // fallback kernel; tests use it to cover it on every geometry)
     int lin_shapes_cur = 0;     // k_pnn_tiles shapes every frame of the current insert call fits
@@ -797,6 +798,7 @@ extern "C" int svr_create(const svr_grid_desc* desc, int device, svr_volume** ou
     svr_volume* v = new svr_volume();
     v->d = *desc;
     if (const char* e = std::getenv("SVR_INSERT_KERNEL")) v->insert_kernel = !std::strcmp(e, "direct") ? 1 : 3;
+    if (const char* e = std::getenv("SVR_TRI_KERNEL")) v->tri_kernel = !std::strcmp(e, "chunk") ? 1 : 0;
 
     v->device = device;
     auto bail = [&](int code) {
@@ -1294,6 +1296,14 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
         } else if (mode == kModeInsert) {
             launch_insert<kModeInsert>(v, vec, skip, box, p, pitch, fstride, w, h, m, fps + k0, cal,
                                        mark, tag, bx, stats);
+        } else if (mode == kModeTrilinear && v->tri_kernel == 0) {
+            // lane = pixel splat (SVR_TRI_KERNEL=chunk keeps the chunk-per-thread k_insert: tests)
+            dim3 grid((h + 7) / 8, m);
+            if (skip)
+                k_tri_warp<true><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, fps + k0, v->d_fan, gd, v->tri, stats);
+            else
+                k_tri_warp<false><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, fps + k0, v->d_fan, gd, v->tri, stats);
+            v->launches++;
         } else if (mode == kModeTrilinear) {
             launch_insert<kModeTrilinear>(v, vec, skip, false, p, pitch, fstride, w, h, m, fps + k0,
                                           cal, mark, tag, nullptr, stats);

@@ -49,6 +49,11 @@ __global__ void __launch_bounds__(256) kern(unsigned long long* g, int iters, un
             atomicAdd(&g[hash32(t * 131u + it) & W28], 1ull);
         }
         if (MODE == 14) acc += g[hash32(t * 131u + it) & W28];
+        // float2 (red.global.add.v2.f32, the trilinear splat's atomic): one lane per sector in a
+        // 1 MiB window; a warp on 32 consecutive pairs (8 sectors); 4 lanes per sector, sectors apart
+        if (MODE == 18) atomicAdd(reinterpret_cast<float2*>(g) + (hash32(t * 131u + it) & ((1u << 17) - 1)), make_float2(1.f, 1.f));
+        if (MODE == 19) atomicAdd(reinterpret_cast<float2*>(g) + (((hash32((t >> 5) * 31u + it) << 5) + lane) & ((1u << 17) - 1)), make_float2(1.f, 1.f));
+        if (MODE == 20) atomicAdd(reinterpret_cast<float2*>(g) + (hash32(t * 131u + it) & W28), make_float2(1.f, 1.f));
         if (MODE == 17) asm volatile("prefetch.global.L2 [%0];" ::"l"(&g[hash32(t * 131u + it) & W28]));
     }
     __syncthreads();
@@ -99,6 +104,9 @@ int main() {
     run<16>("red64_2GiB_pf32", g, sink, blocks, iters);
     run<14>("ld64_2GiB", g, sink, blocks, iters);
     run<17>("pf_2GiB", g, sink, blocks, iters);
+    run<18>("redf2_spread_1M", g, sink, blocks, iters);
+    run<19>("redf2_coal_1M", g, sink, blocks, iters);
+    run<20>("redf2_2GiB", g, sink, blocks, iters);
     cudaError_t e = cudaDeviceSynchronize();
     printf("status %s, SMs %d\n", cudaGetErrorString(e), sms);
     return e == cudaSuccess ? 0 : 1;
