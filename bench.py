@@ -317,7 +317,7 @@ def trilinear_extras(wl, grid, frames, stream, insert_ms, nsample=16, nlat=40):
         del wt
     u8m = float(np.mean(u8))
     alg = wl.nframes * (wl.w * wl.h + 16.0 * u8m)
-    out = {"roofline": {"bound": "hbm", "kernel": "k_insert<trilinear> (K1t)", "unit": "GB/s",
+    out = {"roofline": {"bound": "hbm", "kernel": "k_tri_warp (K1t)", "unit": "GB/s",
                         "achieved": alg / (insert_ms / 1e3) / 1e9, "peak": hbm,
                         "frac": alg / (insert_ms / 1e3) / 1e9 / hbm,
                         "bytes_model": "W*H + 16*U8 per frame (f32 wsum + weight RMW of each distinct "

@@ -7,7 +7,7 @@ import pytest
 
 import paper_2412_00058_b200 as pkg
 from oracle import oracle as O
-from paper_2412_00058_b200 import synth
+from paper_2412_00058_b200 import _abi, synth
 
 pytestmark = pytest.mark.gpu
 
@@ -308,6 +308,44 @@ def test_trilinear_tolerance():
     assert (wt > 0).sum() > 10000
     np.testing.assert_allclose(wt, ref.weight64, rtol=1e-5, atol=0)
     np.testing.assert_allclose(ws, ref.wsum64, rtol=1e-5, atol=0)
+
+@pytest.mark.parametrize("kernel", ["warp", "chunk"])
+@pytest.mark.parametrize("case", ["ragged_linear", "skip_zero", "fan"])
+def test_trilinear_splat_kernels_edge_cases(case, kernel, monkeypatch):
+    """Both trilinear splats (k_tri_warp: lane = pixel with the x + 1 corners handed to the next
+    lane; SVR_TRI_KERNEL=chunk: k_insert, a 16-pixel chunk per thread) against the oracle's fp64 sum
+    of the same contributions at 1e-5 relative, no absolute floor: a row length that is not a
+    multiple of 32 (idle lanes in the last segment), pixels clipped at every grid face, skip_zero
+    (holes break the hand-over chain) and a convex fan (neighbouring lanes rarely on neighbouring
+    voxels: no hand-over); pixel counters equal the oracle's."""
+    import dataclasses
+    if kernel == "chunk":
+        monkeypatch.setenv("SVR_TRI_KERNEL", "chunk")
+    else:
+        monkeypatch.delenv("SVR_TRI_KERNEL", raising=False)
+    if case == "fan":
+        wl = dataclasses.replace(synth.small_fan(), accum=_abi.ACC_TRILINEAR)
+    else:
+        wl = dataclasses.replace(synth.small_linear(w=70, h=45, nframes=8), accum=_abi.ACC_TRILINEAR)
+    frames = wl.frames_np().copy()
+    skip = case == "skip_zero"
+    if skip:
+        frames[:, ::3, 5:40:2] = 0
+        frames[:, 7, :] = 0
+    grid = _grid(wl)
+    grid.insert_frames(frames, wl.poses, wl.calib, skip_zero=skip)
+    ref = O.OracleGrid.for_workload(wl)
+    ref.insert_trilinear_f64(frames, wl.poses, wl.calib, skip_zero=skip)
+    ws, wt = grid.trilinear()
+    assert (wt > 0).sum() > 2000
+    np.testing.assert_allclose(wt, ref.weight64, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(ws, ref.wsum64, rtol=1e-5, atol=0)
+    st = grid.stats()
+    assert st["pixels_inserted"] + st["pixels_oob"] + st["pixels_skipped_zero"] == frames.size
+    if skip:
+        assert st["pixels_skipped_zero"] == int((frames == 0).sum())
+    grid.close()
+
 
 def test_footprint_counts():
     wl = synth.small_linear(nframes=5)

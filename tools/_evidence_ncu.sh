@@ -7,5 +7,5 @@ python tools/profile_bench_step.py 2 > gpurun_out/plain.log 2>&1 && \
 python tools/profile_config.py cfg3 2 > gpurun_out/p3.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_fan_tiles|k_fan_desc" -s 2 -c 2 -o gpurun_out/r2_fan python tools/profile_config.py cfg3 2 > gpurun_out/ncu_f.log 2>&1
 python tools/profile_config.py cfg5 2 > gpurun_out/p5.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_insert" -s 1 -c 1 -o gpurun_out/r2_tri python tools/profile_config.py cfg5 2 > gpurun_out/ncu_t.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"k_insert|k_tri_warp" -s 1 -c 1 -o gpurun_out/r2_tri python tools/profile_config.py cfg5 2 > gpurun_out/ncu_t.log 2>&1
 ls -la gpurun_out/r2_*
