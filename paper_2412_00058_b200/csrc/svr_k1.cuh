@@ -36,12 +36,6 @@
 #ifndef SVR_K1_ORDER
 #define SVR_K1_ORDER 0  // k_pnn_tiles tile order: 0 frame-major, 1 tile-major (frames fastest)
 #endif
-#ifndef SVR_FLUSH_FMA
-#define SVR_FLUSH_FMA 0  // k_pnn_tiles flush: 1 = word split on the FMA pipe, 2 = + plane offsets by IMAD
-#endif
-#ifndef SVR_FLUSH_PIPE
-#define SVR_FLUSH_PIPE 0  // k_pnn_tiles flush: next position's table words loaded ahead; ceil by FADD.RU
-#endif
 #ifndef SVR_FLUSH_UNROLL
 #define SVR_FLUSH_UNROLL 1  // k_pnn_tiles flush loop unroll
 #endif
@@ -282,15 +276,6 @@ __device__ __forceinline__ void red_word(unsigned long long addr, uint32_t v) {
         "{\n\t.reg .b32 hi, lo;\n\t.reg .b64 w;\n\t"
         "shr.u32 hi, %1, 20;\n\tand.b32 lo, %1, 1048575;\n\t"
         "mov.b64 w, {lo, hi};\n\tred.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v) : "memory");
-}
-
-// the same with the split on the FMA pipe (hi = v * 2^12 >> 32, lo = v - hi * 2^20; k12 = 4096 and
-// km20 = -2^20 opaque to ptxas, which would otherwise strength-reduce to ALU shifts)
-__device__ __forceinline__ void red_word_nz_fma(unsigned long long addr, uint32_t v, uint32_t k12, uint32_t km20) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .b32 hi, lo;\n\t.reg .b64 w;\n\t"
-        "setp.ne.u32 p, %1, 0;\n\tmul.hi.u32 hi, %1, %2;\n\tmad.lo.u32 lo, hi, %3, %1;\n\t"
-        "mov.b64 w, {lo, hi};\n\t@p red.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v), "r"(k12), "r"(km20) : "memory");
 }
 
 // the same, predicated on v != 0 inside the asm (no branch around the RED)
@@ -590,61 +575,19 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 float yf = (float)yr;
                 const int dti = kTabStr * R;
                 const uint32_t dgo = (uint32_t)R * nx8;
-#if SVR_FLUSH_FMA
-                const uint32_t k12 = s_fr.pad, km20 = 0u - (k12 << 8), nsxy8 = 0u - sxy8;
-#endif
-#if SVR_FLUSH_PIPE
-                // software-pipelined: the next position's slots are read (and zeroed) before this
-                // position's REDs, so the LDS latency overlaps the previous position's tail
-                uint32_t n0 = 0u, n1 = 0u;
-                if (yr < Y) {
-                    n0 = s_tab[ti];
-                    n1 = s_tab[ti + TG::kPlane];
-                    s_tab[ti] = 0u;
-                    s_tab[ti + TG::kPlane] = 0u;
-                }
-#endif
 #pragma unroll kFlushUnroll
                 for (int y = yr; y < Y; y += R) {
-#if SVR_FLUSH_PIPE
-                    const uint32_t v0 = n0, v1 = n1;
-                    if (y + R < Y) {
-                        n0 = s_tab[ti + dti];
-                        n1 = s_tab[ti + dti + TG::kPlane];
-                        s_tab[ti + dti] = 0u;
-                        s_tab[ti + dti + TG::kPlane] = 0u;
-                    }
-                    // ceil by a round-up add of 1.5 * 2^23 (FADD.RU, full rate) instead of F2I.CEIL:
-                    // the sum lies in [2^23, 2^24) (ulp 1) for |t| < 2^22, so it rounds up to
-                    // 1.5 * 2^23 + ceil(t) exactly
-                    const uint32_t k = __float_as_uint(__fadd_ru(fmaf(p2, yf, ttx), 12582912.0f)) - 0x4b400000u;
-#else
                     const uint32_t v0 = s_tab[ti], v1 = s_tab[ti + TG::kPlane];
                     s_tab[ti] = 0u;
                     s_tab[ti + TG::kPlane] = 0u;
                     const uint32_t k = (uint32_t)(int)ceilf(fmaf(p2, yf, ttx));  // k - kmin >= 0
-#endif
-#if SVR_FLUSH_FMA >= 2
-                    // plane 0 holds z = k + o, plane 1 z = k + 1 - o (o = parity offset): offsets by IMAD
-                    const uint32_t o = (k ^ zpar) & 1u;
-                    const uint32_t kb = k * sxy8 + go;
-                    const unsigned long long ga0 = fbase + (o * sxy8 + kb), ga1 = fbase + (o * nsxy8 + (kb + sxy8));
-                    red_word_nz_fma(ga0, v0, k12, km20);
-                    red_word_nz_fma(ga1, v1, k12, km20);
-#else
                     const bool odd = ((k ^ zpar) & 1u) != 0u;
                     const unsigned long long a0 = fbase + (k * sxy8 + go);
                     // per slot: an empty slot's voxel may lie outside the slab (face tiles), and a
                     // RED of 0 would still pull its line into L2 and write it back
                     const uint32_t vlo = odd ? v1 : v0, vhi = odd ? v0 : v1;
-#if SVR_FLUSH_FMA
-                    red_word_nz_fma(a0, vlo, k12, km20);
-                    red_word_nz_fma(a0 + sxy8, vhi, k12, km20);
-#else
                     red_word_nz(a0, vlo);
                     red_word_nz(a0 + sxy8, vhi);
-#endif
-#endif
                     ti += dti;
                     go += dgo;
                     yf += Rf;
