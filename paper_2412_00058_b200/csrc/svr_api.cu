@@ -1298,7 +1298,12 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
                                        mark, tag, bx, stats);
         } else if (mode == kModeTrilinear && v->tri_kernel == 0) {
             // lane = pixel splat (SVR_TRI_KERNEL=chunk keeps the chunk-per-thread k_insert: tests)
-            dim3 grid((h + 7) / 8, m);
+            // small batches (the per-frame path): rows split into column ranges so that every SM
+            // gets work (a 480-row frame alone is 60 CTAs)
+            const int row_ctas = (h + 7) / 8;
+            int nsplit = 1;
+            while (nsplit < 8 && (long long)row_ctas * m * nsplit < 2ll * v->num_sms && 64 * nsplit < w) nsplit *= 2;
+            dim3 grid(row_ctas, m, nsplit);
             if (skip)
                 k_tri_warp<true><<<grid, 256, 0, v->stream>>>(p, pitch, fstride, w, h, fps + k0, v->d_fan, gd, v->tri, stats);
             else
