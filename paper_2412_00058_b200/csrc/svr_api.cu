@@ -159,7 +159,7 @@ struct svr_volume {
     int insert_kernel = 3;      // SVR_INSERT_KERNEL=direct: every PNN insert through k_insert (the
                                 // fallback kernel; tests use it to cover it on every geometry)
     int lin_shapes_cur = 0;     // k_pnn_tiles shapes every frame of the current insert call fits
-    int tiles_occ[16] = {0};    // k_pnn_tiles resident CTAs per SM, per <shape, box, z1> (lazy)
+    int tiles_occ[32] = {0};    // k_pnn_tiles resident CTAs per SM, per <shape, box, z1, skip> (lazy)
     TileDesc* d_desc = nullptr; // k_pnn_tiles per-tile descriptors
     long long desc_cap = 0;
     TileFrame* d_frc = nullptr; // k_pnn_tiles per-frame constants
@@ -1120,12 +1120,12 @@ static int launch_fan(svr_volume* v, bool box, const uint8_t* px, long long pitc
 }
 
 // K1 for linear probes: k_pnn_tiles (persistent over the launch's tiles) + the exact pass.
-template <int NCH, int NW, bool kBox, bool kZ1>
+template <int NCH, int NW, bool kBox, bool kZ1, bool kSkip>
 static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
-    const int slot = (NCH == 2) + 2 * (NW == 2) + 4 * kBox + 8 * kZ1;
+    const int slot = (NCH == 2) + 2 * (NW == 2) + 4 * kBox + 8 * kZ1 + 16 * kSkip;
     if (!v->tiles_occ[slot]) {
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pnn_tiles<NCH, NW, kBox, kZ1>, 32 * NW, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pnn_tiles<NCH, NW, kBox, kZ1, kSkip>, 32 * NW, 0));
         v->tiles_occ[slot] = std::max(1, occ);
     }
     const long long ctas = std::min<long long>(ta.ntiles, (long long)v->num_sms * v->tiles_occ[slot]);
@@ -1138,7 +1138,7 @@ static int launch_tiles_t(svr_volume* v, const TilesArgs& ta) {
     } else {
         k_tile_desc<NCH, NW, kZ1><<<(unsigned)((ta.ntiles + 127) / 128), 128, 0, v->stream>>>(ta, const_cast<TileDesc*>(ta.desc));
     }
-    k_pnn_tiles<NCH, NW, kBox, kZ1><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
+    k_pnn_tiles<NCH, NW, kBox, kZ1, kSkip><<<(unsigned)ctas, 32 * NW, 0, v->stream>>>(ta);
     v->launches += 2;
     return SVR_OK;
 }
@@ -1166,7 +1166,21 @@ static int pick_shape(int shapes, int w, int h, int nframes, int num_sms) {
     return best >= 0 && (shapes & kFitZ1) ? best | kShapeZ1 : best;
 }
 
-static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, long long pitch,
+template <bool kBox, bool kSkip>
+static int launch_tiles_s(svr_volume* v, int shape, const TilesArgs& ta) {
+    switch (shape & 7) {  // bits 0-1: tile shape, bit 2 (kShapeZ1): the kZ1 walk
+        case 0: return launch_tiles_t<4, 4, kBox, false, kSkip>(v, ta);
+        case 1: return launch_tiles_t<2, 4, kBox, false, kSkip>(v, ta);
+        case 2: return launch_tiles_t<4, 2, kBox, false, kSkip>(v, ta);
+        case 3: return launch_tiles_t<2, 2, kBox, false, kSkip>(v, ta);
+        case 4: return launch_tiles_t<4, 4, kBox, true, kSkip>(v, ta);
+        case 5: return launch_tiles_t<2, 4, kBox, true, kSkip>(v, ta);
+        case 6: return launch_tiles_t<4, 2, kBox, true, kSkip>(v, ta);
+        default: return launch_tiles_t<2, 2, kBox, true, kSkip>(v, ta);
+    }
+}
+
+static int launch_tiles(svr_volume* v, int shape, bool box, bool skip, const uint8_t* px, long long pitch,
                         long long fstride, int w, int h, int m, const FrameParams* fps, int* boxes,
                         ull* stats) {
     TilesArgs ta;
@@ -1188,28 +1202,13 @@ static int launch_tiles(svr_volume* v, int shape, bool box, const uint8_t* px, l
     if (int e = ensure_desc(v, ta.ntiles, m)) return e;
     ta.desc = v->d_desc;
     ta.frc = v->d_frc;
-    switch ((shape & 7) + 8 * box) {
-        case 0: return launch_tiles_t<4, 4, false, false>(v, ta);
-        case 1: return launch_tiles_t<2, 4, false, false>(v, ta);
-        case 2: return launch_tiles_t<4, 2, false, false>(v, ta);
-        case 3: return launch_tiles_t<2, 2, false, false>(v, ta);
-        case 4: return launch_tiles_t<4, 4, false, true>(v, ta);
-        case 5: return launch_tiles_t<2, 4, false, true>(v, ta);
-        case 6: return launch_tiles_t<4, 2, false, true>(v, ta);
-        case 7: return launch_tiles_t<2, 2, false, true>(v, ta);
-        case 8: return launch_tiles_t<4, 4, true, false>(v, ta);
-        case 9: return launch_tiles_t<2, 4, true, false>(v, ta);
-        case 10: return launch_tiles_t<4, 2, true, false>(v, ta);
-        case 11: return launch_tiles_t<2, 2, true, false>(v, ta);
-        case 12: return launch_tiles_t<4, 4, true, true>(v, ta);
-        case 13: return launch_tiles_t<2, 4, true, true>(v, ta);
-        case 14: return launch_tiles_t<4, 2, true, true>(v, ta);
-        default: return launch_tiles_t<2, 2, true, true>(v, ta);
-    }
+    return skip ? (box ? launch_tiles_s<true, true>(v, shape, ta) : launch_tiles_s<false, true>(v, shape, ta))
+                : (box ? launch_tiles_s<true, false>(v, shape, ta) : launch_tiles_s<false, false>(v, shape, ta));
 }
 
 // Launch over frames resident in device memory, chunked to the grid.y limit.
-//   PNN insert, no skip_zero: linear probes k_tile_desc + k_pnn_tiles (svr_k1.cuh); convex fans
+//   PNN insert: linear probes k_tile_desc + k_pnn_tiles (svr_k1.cuh; skip_zero as its kSkip
+//   variant); no skip_zero: convex fans
 //   k_fan_desc + k_fan_tiles (svr_fan.cuh, 32-byte aligned rows of whole 128-sample tiles) or
 //   else k_pnn_plane; each + k_pnn_work (the exact pass).  k_insert: skip_zero, geometries the
 //   tiles refuse, SVR_INSERT_KERNEL=direct (tests), footprint and trilinear.
@@ -1222,7 +1221,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
     const bool direct = v->insert_kernel == 1;
     // linear probes: k_pnn_tiles (reads each row segment with 32-byte loads)
     const bool vec32 = ((uintptr_t)px % 32 == 0) && (pitch % 32 == 0) && (n == 1 || fstride % 32 == 0);
-    const int shape = (mode == kModeInsert && !skip && !direct && cal.probe == SVR_PROBE_LINEAR && vec32)
+    const int shape = (mode == kModeInsert && !direct && cal.probe == SVR_PROBE_LINEAR && vec32)
                           ? pick_shape(v->lin_shapes_cur, w, h, n, v->num_sms)
                           : -1;
     // convex fan: tables of packed (count << 20 | sum) slots hold at most 4095 pixels: guaranteed
@@ -1239,7 +1238,8 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
         int* bx = boxes ? boxes + 6 * k0 : nullptr;
         // the deferred-chunk pass is grid-strided over a worklist of a few entries per frame:
         // a single frame must not pay for launching thousands of idle CTAs
-        const int work_ctas = std::min(SVR_WORK_CTAS_PER_SM * v->num_sms, std::max(16, 8 * m));
+        // (skip_zero sends every chunk with both zero and non-zero pixels there: more CTAs)
+        const int work_ctas = std::min((skip ? 8 : SVR_WORK_CTAS_PER_SM) * v->num_sms, std::max(16, 8 * m));
         const GridDev gd = dev_grid(v->d);
         if (shape >= 0 || fan_tiles) {
             // k_pnn_tiles / k_fan_tiles defer whole chunks with no overflow path: room for every chunk
@@ -1258,7 +1258,7 @@ static int insert_device(svr_volume* v, int mode, const uint8_t* px, long long p
             if (fan_tiles) {
                 if (int e = launch_fan(v, box, p, pitch, fstride, w, h, m, fps + k0, cal, bx, stats)) return e;
             } else {
-                if (int e = launch_tiles(v, shape, box, p, pitch, fstride, w, h, m, fps + k0, bx, stats)) return e;
+                if (int e = launch_tiles(v, shape, box, skip, p, pitch, fstride, w, h, m, fps + k0, bx, stats)) return e;
             }
             if (box)
                 k_pnn_work<true, true><<<work_ctas, 256, 0, v->stream>>>(

@@ -167,10 +167,19 @@ struct __align__(16) TileFrame {
 };
 static_assert(sizeof(TileFrame) == 96, "TileFrame is staged as 6 x 16 bytes");
 
-__device__ __forceinline__ void push_work(const TilesArgs& ta, int f, int row, int cc) {
+__device__ __forceinline__ void push_work(const TilesArgs& ta, int f, int row, int cc, uint32_t mask = 0xffffu) {
     // the host sizes the list for every chunk of the launch, so it cannot overflow
     const unsigned int slot = atomicAdd(ta.work_n, 1u);
-    ta.work[slot] = work_entry(f, row, cc, 0xffffu);
+    ta.work[slot] = work_entry(f, row, cc, mask);
+}
+
+// bit j set where pixel j of the chunk is zero (skip_zero)
+__device__ __forceinline__ uint32_t zero_mask16(const uint32_t (&w)[4]) {
+    uint32_t m = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)  // bytes 0..3 of __vcmpeq4's 0xff / 0x00 -> bits 24..27 of the product
+        m |= (((__vcmpeq4(w[i], 0u) & 0x01010101u) * 0x01020408u) >> 24 & 0xfu) << (4 * i);
+    return m;
 }
 
 template <int NCH, int NW, bool kZ1>
@@ -286,17 +295,22 @@ __device__ __forceinline__ void red_word_nz(unsigned long long addr, uint32_t v)
         "mov.b64 w, {lo, hi};\n\t@p red.relaxed.gpu.global.add.u64 [%0], w;\n\t}" ::"l"(addr), "r"(v) : "memory");
 }
 
-template <int NCH, int NW, bool kBox, bool kZ1>
+// kSkip (skip_zero): a chunk of 16 zero pixels adds nothing and is counted skipped
+// whatever its position; a chunk with some zero pixels goes to the exact pass with the mask of its
+// non-zero pixels (per-pixel counters and boxes there), its zeros counted skipped here.
+template <int NCH, int NW, bool kBox, bool kZ1, bool kSkip = false>
 __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TILES_MINB) k_pnn_tiles(const TilesArgs ta) {
     constexpr int NT = 32 * NW, TROWS = 32 * NW, TCOLS = 16 * NCH;
     using TG = TabGeom<NW>;
     __shared__ __align__(16) uint32_t s_tab[TG::kWords];
     __shared__ TileFrame s_frs[3];       // ring (tiles i, i + 1, i + 2): frame constants
     __shared__ TileDesc s_desc[3];       //   and descriptors, cp.async-staged
-    __shared__ unsigned int s_cnt[2];    // chunks counted out of bounds / deferred (rare)
+    // chunks counted out of bounds / deferred (rare); skip_zero: all-zero chunks, zero pixels of
+    // mixed chunks, and those of them in chunks walked here
+    __shared__ unsigned int s_cnt[5];
     __shared__ unsigned long long s_px;  // pixels of this CTA's tiles
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < 2) s_cnt[tid] = 0u;
+    if (tid < 5) s_cnt[tid] = 0u;
     if (tid == 0) s_px = 0ull;
     for (int i = tid; i < TG::kWords / 4; i += NT)
         reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -440,13 +454,48 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         auto chunk_u = [&](int c, int k) -> long long {
             return dsc.Ut[k] + (long long)rrel * s_fr.Dr[k] + (long long)(16 * c) * s_fr.Dc[k];
         };
+        // (kSkip) chunks with zero pixels: all zero -> skipped; mixed -> walked with per-pixel
+        // counts in inside tiles of a batch insert, else sent to the exact pass with their mask
+        // (boxes and face counters per pixel there)
+        uint32_t handled = 0u, zmr[kSkip ? NCH : 1] = {};
+        if constexpr (kSkip) {
+            if (act) {
+                uint32_t nskip = 0u, nzero = 0u, nzwalk = 0u;
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const uint32_t zm = zero_mask16(wd[c]);
+                    zmr[c] = zm;
+                    if (zm == 0xffffu) {
+                        handled |= 1u << c;
+                        ++nskip;
+                    } else if (zm != 0u) {
+                        nzero += __popc(zm);
+                        if (kBox || !tok || !tin) {
+                            handled |= 1u << c;
+                            push_work(ta, f, row, (c0t >> 4) + c, zm ^ 0xffffu);
+                            atomicAdd(&s_cnt[1], 1u);
+                        } else {
+                            nzwalk += __popc(zm);
+                        }
+                    }
+                    if ((handled >> c) & 1u) {
+                        wd[c][0] = wd[c][1] = wd[c][2] = wd[c][3] = 0u;  // walked, adds nothing
+                        zmr[c] = 0u;
+                    }
+                }
+                if (nskip) atomicAdd(&s_cnt[2], nskip);
+                if (nzero) atomicAdd(&s_cnt[3], nzero);
+                if (nzwalk) atomicAdd(&s_cnt[4], nzwalk);
+            }
+        }
         // per-chunk write mask: a chunk goes into the table when its whole index range lies inside
         // the grid / slab; wholly outside -> counted out of bounds; straddling -> exact pass
-        uint32_t wmask = act && tok ? (1u << NCH) - 1u : 0u;
+        uint32_t wmask = act && tok ? ((1u << NCH) - 1u) & ~handled : 0u;
         if (act && (!tok || !tin)) {
             const int clo[3] = {0, 0, g.zb}, chi[3] = {g.nx - 1, g.ny - 1, g.zb + g.nzl - 1};
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
+                if (kSkip && ((handled >> c) & 1u)) continue;
                 bool inb = true, out = false;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -470,7 +519,9 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                 }
             }
         }
-        if (tok && warp < S) {
+        // (kSkip: a warp whose rows are all zero / out of bounds has nothing to walk -- the rows
+        // outside a segmented frame's band)
+        if (tok && warp < S && (!kSkip || __any_sync(0xffffffffu, wmask != 0u))) {
             const uint32_t e0 = s_fr.E[0], e1 = s_fr.E[1], e2 = s_fr.E[2], sx = s_fr.sx, sy = s_fr.sy;
             const uint32_t tie2 = 2u * s_fr.te2;
             // (kZ1: 1 / e for the post-carry residues; MUFU accuracy suffices, see carry_residue)
@@ -491,8 +542,14 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             for (int c = 0; c < NCH; ++c) {
                 if (c > 0) tile_step<TG::kBit>(w0, w1, w2, a, e0, e1, e2, sx, sy);
                 const uint32_t o20 = (wmask >> c) & 1u ? 0x00100000u : 0u;
+                // table word of pixel j (kSkip: a zero pixel of a mixed chunk adds no count)
+                const uint32_t zmc = kSkip ? zmr[c] : 0u;
+                auto pw = [&](int j) -> uint32_t {
+                    const uint32_t oj = kSkip && ((zmc >> j) & 1u) ? 0u : o20;
+                    return px_word(wd[c][j >> 2], j & 3, oj);
+                };
                 uint32_t tmin = min(w0, min(w1, w2));
-                red_shared(a, px_word(wd[c][0], 0, o20));
+                red_shared(a, pw(0));
                 if (kZ1) {
                     // at most one y and one z carry in the chunk: the z move is the fixed step to
                     // the other parity plane (an add on the FMA pipe instead of an ALU XOR)
@@ -504,7 +561,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                     for (int j = 1; j < kChunk; ++j) {
                         tile_step_z1(w0, w1, w2, a, e0, e1, e2, sx, sy, dz);
                         tmin = min(tmin, w0);
-                        red_shared(a, px_word(wd[c][j >> 2], j & 3, o20));
+                        red_shared(a, pw(j));
                     }
                     // (only where the axis carried: w wrapped below its chunk-start value)
                     const uint32_t ry = w1 < w1s ? carry_residue(w1, e1, rc1) : 0xffffffffu;
@@ -515,7 +572,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                     for (int j = 1; j < kChunk; ++j) {
                         tile_step<TG::kBit>(w0, w1, w2, a, e0, e1, e2, sx, sy);
                         tmin = min(tmin, min(w0, min(w1, w2)));
-                        red_shared(a, px_word(wd[c][j >> 2], j & 3, o20));
+                        red_shared(a, pw(j));
                     }
                 }
                 const bool tie = o20 != 0u && tmin < tie2;
@@ -523,14 +580,15 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
                     if (tie) {
                         uint32_t v0, v1, v2, ua;  // state at the chunk's pixel 0 (= the walk's)
                         walk_state(chunk_u(c, 0), chunk_u(c, 1), chunk_u(c, 2), s_fr, X0, Y0, tab, (uint32_t)TG::kBit, v0, v1, v2, ua);
-                        red_shared(ua, 0u - px_word(wd[c][0], 0, o20));
+                        red_shared(ua, 0u - pw(0));
 #pragma unroll
                         for (int j = 1; j < kChunk; ++j) {  // (unrolled: wd stays in registers)
                             tile_step<TG::kBit>(v0, v1, v2, ua, e0, e1, e2, sx, sy);
-                            red_shared(ua, 0u - px_word(wd[c][j >> 2], j & 3, o20));
+                            red_shared(ua, 0u - pw(j));
                         }
-                        push_work(ta, f, row, (c0t >> 4) + c);
+                        push_work(ta, f, row, (c0t >> 4) + c, zmc ^ 0xffffu);
                         atomicAdd(&s_cnt[1], 1u);
+                        if (kSkip && zmc) atomicSub(&s_cnt[4], (unsigned int)__popc(zmc));  // (deferred after all)
                     }
                 }
                 if (kBox && o20 != 0u && !tie) {
@@ -558,8 +616,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             tile_rows(ty, Sn, rown, actn, rowcn);
             load_rows(f, tx, rowcn, wd);
         }
-        __syncthreads();  // table complete
-        if (tok) {
+        // table complete (kSkip: a tile no thread wrote to has nothing to flush)
+        bool any_written = true;
+        if constexpr (kSkip) any_written = __syncthreads_or(wmask != 0u) != 0;
+        else __syncthreads();
+        if (tok && any_written) {
             // flush + zero: thread (x, yr) = (tid mod X, tid div X) takes column x of the table
             // rows yr, yr + R, ... (R = NT div X rows per pass; fixed per thread, so no wrap logic)
             const float p1 = s_fr.p1, p2 = s_fr.p2;
@@ -600,9 +661,12 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
     if (kBox && cur_f >= 0) flush_box(bb, ta.boxes + 6 * cur_f);
     if (tid == 0) {  // (after the loop's last barrier: s_cnt is final)
         const ull oob = 16ull * s_cnt[0], def = s_cnt[1], n_px = s_px;
-        // every pixel of the CTA's tiles is inserted here unless counted out of bounds or deferred
-        // (k_pnn_work counts the deferred chunks' pixels)
-        if (n_px > oob + 16ull * def) atomicAdd(&ta.stats[kStInserted], n_px - oob - 16ull * def);
+        const ull skp = kSkip ? 16ull * s_cnt[2] : 0ull, zwk = kSkip ? (ull)s_cnt[4] : 0ull;
+        // every pixel of the CTA's tiles is inserted here unless counted out of bounds, skipped
+        // or deferred (k_pnn_work counts the deferred chunks' pixels)
+        if (n_px > oob + 16ull * def + skp + zwk)
+            atomicAdd(&ta.stats[kStInserted], n_px - oob - 16ull * def - skp - zwk);
+        if (kSkip && skp + s_cnt[3]) atomicAdd(&ta.stats[kStSkipped], skp + (ull)s_cnt[3]);
         if (oob) atomicAdd(&ta.stats[kStOob], oob);
         if (def) atomicAdd(&ta.stats[kStDeferred], def);
         if (ntiles_cta) atomicAdd(&ta.stats[kStTiles], (ull)ntiles_cta);

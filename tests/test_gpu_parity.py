@@ -309,6 +309,41 @@ def test_trilinear_tolerance():
     np.testing.assert_allclose(wt, ref.weight64, rtol=1e-5, atol=0)
     np.testing.assert_allclose(ws, ref.wsum64, rtol=1e-5, atol=0)
 
+@pytest.mark.parametrize("want_boxes", [False, True])
+@pytest.mark.parametrize("slab", [None, (60, 90)])
+def test_skip_zero_through_tile_kernel(want_boxes, slab):
+    """skip_zero on the K1 tile kernel (k_pnn_tiles<kSkip>): cfg2 geometry, frames cut to a band of
+    rows (whole chunks, warps and tiles of zeros), zeros sprinkled inside the band (mixed chunks:
+    walked with per-pixel counts in a batch insert, sent to the exact pass with their mask when
+    boxes are wanted or the tile meets a slab face) and a zero run crossing chunk borders.
+    Accumulators, per-frame boxes and the inserted / out-of-bounds / skipped counters equal the
+    oracle's, on the whole grid and on a z-slab whose faces cut the frames."""
+    wl = synth.cfg2(nframes=24)
+    frames = wl.frames_np().copy()
+    frames[:, :150, :] = 0
+    frames[:, 300:, :] = 0
+    rng = np.random.default_rng(5)
+    frames[rng.random(frames.shape) < 0.004] = 0
+    frames[:, 200, 37:90] = 0
+    frames[3] = 0  # a frame with nothing to insert
+    kw = {} if slab is None else {"z_range": slab}
+    grid = _grid(wl, **kw)
+    ref = O.OracleGrid.for_workload(wl, z_range=slab)
+    rboxes = ref.insert_frames(frames, wl.poses, wl.calib, skip_zero=True)
+    if want_boxes:
+        boxes, _ = grid.insert_frames(frames, wl.poses, wl.calib, skip_zero=True, want_boxes=True)
+        assert [b.as_tuple() for b in boxes] == [b.as_tuple() for b in rboxes]
+    else:
+        grid.insert_frames(frames, wl.poses, wl.calib, skip_zero=True)
+    _assert_acc(grid, ref)
+    st = grid.stats()
+    assert st["tiles_table"] > 0, "the insert did not go through k_pnn_tiles"
+    assert st["pixels_skipped_zero"] == int((frames == 0).sum()) == ref.stats["skipped_zero"]
+    assert st["pixels_inserted"] == ref.stats["inserted"]
+    assert st["pixels_oob"] == ref.stats["oob"]
+    grid.close()
+
+
 @pytest.mark.parametrize("kernel", ["warp", "chunk"])
 @pytest.mark.parametrize("case", ["ragged_linear", "skip_zero", "fan"])
 def test_trilinear_splat_kernels_edge_cases(case, kernel, monkeypatch):
