@@ -332,25 +332,37 @@ def trilinear_extras(wl, grid, frames, stream, insert_ms, nsample=16, nlat=40):
         b.record(stream)
         torch.cuda.synchronize()
     out["render_all_columns_ms"] = a.elapsed_time(b)
-    # per-frame: one frame's splat + the render of its dirty columns (call by call)
-    lat = []
+    # per-frame: one frame's splat + the render of its dirty columns, as one CUDA-graph replay
+    # (svr_frame_step) and call by call
     mid = live[len(live) // 2]
-    with torch.cuda.stream(stream):
-        for j in range(nlat + 3):
-            k = mid + j
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            grid.insert_frames(frames[k:k + 1], wl.poses[k:k + 1], wl.calib)
-            if not boxes[k].empty():
-                grid.render_coronal(boxes[k], rp, 0)
-            e1.record(stream)
-            e1.synchronize()
-            if j >= 3:
-                lat.append(e0.elapsed_time(e1))
-    lat.sort()
+
+    def frame_lat(graph):
+        lat = []
+        with torch.cuda.stream(stream):
+            for j in range(nlat + 3):
+                k = mid + j
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                if graph:
+                    grid.frame_step(frames[k], wl.poses[k:k + 1], wl.calib, 1, rp)
+                else:
+                    grid.insert_frames(frames[k:k + 1], wl.poses[k:k + 1], wl.calib)
+                    if not boxes[k].empty():
+                        grid.render_coronal(boxes[k], rp, 0)
+                e1.record(stream)
+                e1.synchronize()
+                if j >= 3:
+                    lat.append(e0.elapsed_time(e1))
+        lat.sort()
+        return lat
+
+    lat, latc = frame_lat(True), frame_lat(False)
     out["latency_ms"] = {"frames": len(lat), "device_p50": lat[len(lat) // 2],
                          "device_p95": lat[int(0.95 * (len(lat) - 1) + 0.5)], "device_max": lat[-1],
-                         "what": "one frame: trilinear splat + depth-band render of its dirty columns"}
+                         "per_call_p50": latc[len(latc) // 2],
+                         "what": "one frame: trilinear splat + depth-band render of its dirty columns as "
+                                 "one CUDA-graph replay (svr_frame_step); per_call: the same kernels "
+                                 "launched call by call"}
     return out
 
 

@@ -190,7 +190,9 @@ int svr_render_coronal(svr_volume* vol, const svr_box* dirty, int32_t fill_radiu
  * is captured on first use (and re-captured when the frame geometry, calibration, render
  * parameters or a region bound changes); px may be host (pageable or pinned) or device memory.
  * Asynchronous; dirty_out (may be NULL) receives the conservative box.  Results are identical to
- * svr_insert_frame + svr_fill_holes + svr_render_coronal over that box.  Pageable host frames are
+ * svr_insert_frame + svr_fill_holes + svr_render_coronal over that box.  On a trilinear volume
+ * (BASELINE cfg5) the step is the splat and the render of the box (+) 1 columns (no fill layer;
+ * fill_radius is ignored).  Pageable host frames are
  * staged before the call returns; pinned host and device frames are read by a copy enqueued on
  * the handle's stream, so px must stay unchanged until the step completes (svr_sync, or an event
  * recorded on the stream after the call). */

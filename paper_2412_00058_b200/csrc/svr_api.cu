@@ -2133,12 +2133,19 @@ static int fg_capture(svr_volume* v, int w, int h, int fr, const svr_calib& c, c
     CK(cudaStreamBeginCapture(v->stream, cudaStreamCaptureModeThreadLocal));
     cudaMemcpyAsync(f.d_fp, f.h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, v->stream);
     cudaMemcpyAsync(f.d_tiles, f.h_tiles, kFgTileBytes, cudaMemcpyHostToDevice, v->stream);
-    int e = insert_device(v, kModeInsert, f.d_frame, w, (long long)w * h, w, h, 1, f.d_fp, dc, false, false,
-                          nullptr, nullptr, 0, v->d_stats);
+    const bool tri = v->tri != nullptr;  // trilinear volume: splat, then depth / band on wsum / weight (no fill layer)
+    int e = insert_device(v, tri ? kModeTrilinear : kModeInsert, f.d_frame, w, (long long)w * h, w, h, 1, f.d_fp, dc,
+                          false, false, nullptr, nullptr, 0, v->d_stats);
     const BoxTiles* bt = (const BoxTiles*)f.d_tiles;
     const ColTiles* dt = (const ColTiles*)(f.d_tiles + sizeof(BoxTiles));
     const ColTiles* mt = dt + 1;
-    if (!e) {
+    if (!e && tri) {
+        k_depth<8, true><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(nullptr, nullptr, g, dt, 1, ylo, yhi, p.fill_mode,
+                                                                        v->r_depth, v->tri);
+        k_band<true><<<grid_1d(f.band_ctas), 128, 0, v->stream>>>(nullptr, nullptr, g, mt, 1, p.median_radius, above,
+                                                                   below, p.fill_mode, v->r_depth, v->r_mdepth,
+                                                                   v->r_mean, v->r_max, v->gt, v->tri);
+    } else if (!e) {
         // 2-plane marches: a single frame's box is shallow in z, short marches cut its latency
         k_fill_warp<2, 1, 8, false><<<grid_1d(f.fill_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, bt, 1, nullptr);
         k_depth<8><<<grid_1d(f.depth_ctas), 128, 0, v->stream>>>(v->acc, v->fill, g, dt, 1, ylo, yhi,
@@ -2172,12 +2179,14 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
                               svr_box* dirty_out) {
     NvtxRange nvtx_("svr_frame_step");
     VOL_CHECK(v);
-    if (!v->acc) return fail(SVR_E_INVALID, "frame step needs a PNN volume");
+    const bool tri = v->tri != nullptr;
+    if (!v->acc && !tri) return fail(SVR_E_INVALID, "frame step needs a volume");
     if (!px || !pose || !p) return fail(SVR_E_INVALID, "NULL argument");
     if (int e = check_calib(c, c ? c->crop_w : 0, c ? c->crop_h : 0)) return e;
     const int w = c->crop_w, h = c->crop_h;
     if (pitch < w) return fail(SVR_E_INVALID, "row pitch %lld < width %d", (long long)pitch, w);
-    if (fill_radius != 1) return fail(SVR_E_INVALID, "the frame graph runs the r = 1 mean fill");
+    if (tri) fill_radius = 0;  // (a trilinear volume has no fill layer: splat + render)
+    else if (fill_radius != 1) return fail(SVR_E_INVALID, "the frame graph runs the r = 1 mean fill");
     if (p->median_radius < 0 || p->median_radius > 2) return fail(SVR_E_INVALID, "median_radius must be 0..2");
     FrameGraph& f = v->fg;
     if (f.done) CK(cudaEventSynchronize(f.done));  // staging of the previous frame consumed
@@ -2185,8 +2194,9 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     Box fb;
     svr_box bd{b.x0 - 1, b.y0 - 1, b.z0 - 1, b.x1 + 1, b.y1 + 1, b.z1 + 1};
     ColTiles ct[2];
+    // (trilinear: the 2x2x2 splat reaches one voxel past the nearest-voxel box: render box + 1)
     const bool any = b.x0 <= b.x1 && clip_box(v, &bd, &fb) &&
-                     render_regions(v, &b, fill_radius, p->median_radius, &ct[0], &ct[1]);
+                     render_regions(v, tri ? &bd : &b, fill_radius, p->median_radius, &ct[0], &ct[1]);
     if (!any) {  // frame entirely outside the slab: a plain insert counts its pixels
         if (dirty_out) *dirty_out = svr_box{1, 1, 1, 0, 0, 0};
         return svr_insert_frames(v, px, pitch, pitch * h, w, h, 1, pose, c, 0, nullptr, nullptr);
@@ -2196,16 +2206,16 @@ extern "C" int svr_frame_step(svr_volume* v, const uint8_t* px, int64_t pitch, c
     bt.ntx = (fb.x1 - fb.x0 + 1 + 29) / 30;  // k_fill_warp<.., 8>: 30 columns x 4 warps of 8 rows
     bt.nty = (fb.y1 - fb.y0 + 1 + 31) / 32;
     bt.first = 0;
-    const long long nf = (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 1) / 2);
+    const long long nf = tri ? 0 : (long long)bt.ntx * bt.nty * ((fb.z1 - fb.z0 + 1 + 1) / 2);
     std::vector<ColTiles> cv{ct[0]}, mv{ct[1]};
     const long long nd = tile_cols(cv, 16), nm = tile_cols(mv);
     FrameParams fpar;
     if (int e = make_params(*pose, prep_ctx(*c, v->d), c->scale_x_mm, c->scale_y_mm, &fpar)) return e;
     // the insert's tile shape is part of the capture: a frame that fits none of the captured
     // shape's tiles is still exact (its tiles take the exact pass) but re-captures once
-    const bool shape_ok = f.shape < 0 ? fpar.lin_fit == 0
-                                      : ((fpar.lin_fit >> (f.shape & 3)) & 1) != 0 &&
-                                            (!(f.shape & kShapeZ1) || (fpar.lin_fit & kFitZ1));
+    const bool shape_ok = tri || (f.shape < 0 ? fpar.lin_fit == 0
+                                              : ((fpar.lin_fit >> (f.shape & 3)) & 1) != 0 &&
+                                                    (!(f.shape & kShapeZ1) || (fpar.lin_fit & kFitZ1)));
     if (!fg_matches(f, w, h, fill_radius, *c, *p, nf, nd, nm) || !shape_ok) {
         v->lin_shapes_cur = fpar.lin_fit;
         if (int e = fg_capture(v, w, h, fill_radius, *c, *p, nf, nd, nm)) return e;

@@ -309,6 +309,42 @@ def test_trilinear_tolerance():
     np.testing.assert_allclose(wt, ref.weight64, rtol=1e-5, atol=0)
     np.testing.assert_allclose(ws, ref.wsum64, rtol=1e-5, atol=0)
 
+def test_frame_step_graph_on_trilinear_volume():
+    """svr_frame_step on a trilinear volume (cfg5 geometry): one CUDA-graph replay per frame =
+    splat + depth / band render of the frame's columns (box + 1: the 2x2x2 splat reaches one voxel
+    past the nearest-voxel box).  The volume equals a batch insert's within the fp32 accumulation
+    order (1e-5 relative, no floor) and the incrementally rendered image equals the oracle's
+    whole-volume render of the GPU's own final volume: every column a frame changes lies inside
+    the region that frame re-renders."""
+    import dataclasses
+    wl = dataclasses.replace(synth.cfg5(nframes=8, dims=(160, 120, 40)), origin=(70.0, 20.0, 9.5))
+    frames = wl.frames_np()
+    rp = synth.render_params(depth_lo_mm=1.0, depth_hi_mm=8.0, band_above_mm=0.6, band_below_mm=0.3)
+    inc = _grid(wl)
+    for k in range(wl.nframes):
+        inc.frame_step(frames[k], wl.poses[k:k + 1], wl.calib, 1, rp)
+    inc.sync()
+    assert inc.stats()["graph_captures"] >= 1
+    ws, wt = inc.trilinear()
+    batch = _grid(wl)
+    batch.insert_frames(frames, wl.poses, wl.calib)
+    ws2, wt2 = batch.trilinear()
+    assert (wt > 0).sum() > 10000
+    np.testing.assert_allclose(wt, wt2, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(ws, ws2, rtol=1e-5, atol=0)
+    mean, mx, dep = inc.read_coronal()
+    ref = O.OracleGrid.for_workload(wl)
+    ref.wsum[...] = ws
+    ref.weight[...] = wt
+    rmean, rmx, rdep = ref.render(rp, fill_radius=0)
+    assert (rdep >= 0).sum() > 500
+    assert np.array_equal(dep, rdep)
+    np.testing.assert_allclose(mean, rmean, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(mx, rmx, rtol=1e-5, atol=0)
+    inc.close()
+    batch.close()
+
+
 @pytest.mark.parametrize("want_boxes", [False, True])
 @pytest.mark.parametrize("slab", [None, (60, 90)])
 def test_skip_zero_through_tile_kernel(want_boxes, slab):
