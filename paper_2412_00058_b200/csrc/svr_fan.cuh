@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(128, SVR_FAN_MINB) k_fan_tiles(const FanArgs f
             const uint32_t zpar = (uint32_t)dsc.zpar;
             const float p1 = dsc.p1, p2 = dsc.p2;
             const int XY = X * Y;
-            const float rX = 1.0f / (float)X;
+            const float rX = __fdividef(1.0f, (float)X);  // (MUFU.RCP suffices: see k_pnn_tiles)
             // y = p / X exactly: the quotients' fractional parts are >= 1/(2X) from an integer
             const int y0 = (int)(((float)tid + 0.5f) * rX);
             int x = tid - y0 * X;

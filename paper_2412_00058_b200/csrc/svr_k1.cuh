@@ -625,7 +625,9 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
             // rows yr, yr + R, ... (R = NT div X rows per pass; fixed per thread, so no wrap logic)
             const float p1 = s_fr.p1, p2 = s_fr.p2;
             const uint32_t sxy8 = (uint32_t)((long long)g.nx * g.ny * 8), nx8 = (uint32_t)g.nx * 8u;
-            const float rX = 1.0f / (float)X;
+            // (MUFU.RCP: its 2^-22 relative error moves the quotients below by < 1e-4, far inside
+            // the 1 / (2 X) margin; the IEEE division's range check and slow path are not needed)
+            const float rX = __fdividef(1.0f, (float)X);
             // exact quotients: (a + 1/2) / X is >= 1/(2X) from an integer for X <= 32
             const int yr = (int)(((float)tid + 0.5f) * rX), R = (int)(((float)NT + 0.5f) * rX);
             const int x = tid - yr * X;
