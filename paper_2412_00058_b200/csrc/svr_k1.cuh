@@ -430,13 +430,14 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? SVR_TILES_MINB : 2 * SVR_TI
         const int b = slot;
         slot = slot == 2 ? 0 : slot + 1;
         ++ntiles_cta;
-        {  // the tile after next is requested now
+        // the tile after next is requested now (only the ten staging threads work out which it is)
+        if (tid < 10) {
             int f2 = f, ty2 = ty, tx2 = tx;
             advance(f2, ty2, tx2);
             advance(f2, ty2, tx2);
             if (t + 2 * tstep < t1) stage(f2, ty2, tx2, b == 0 ? 2 : b - 1);
-            commit();
         }
+        commit();
         const TileFrame& s_fr = s_frs[b];
         const TileDesc& dsc = s_desc[b];
         const int c0t = tx * TCOLS, r0t = ty * TROWS;
